@@ -1,0 +1,245 @@
+// nucleus_kernel.cuh — fused Beta-cut nucleus sampler (Alg. 3, PAPER.md:216-239;
+// SPEC.md:437-445) and its Gumbel-max sibling, with the
+// top-p membership test of SPEC.md:440,464 fused in.
+//
+// Per row, one cluster:
+//   1. TMA-load the logit slice into shared memory (kept there: x is needed again).
+//   2. Registers: xt_i = x_i + G_i, G_i = u_i^(1/alpha) (Beta) or -log(-log u_i)
+//      (Gumbel), u_i from Philox4x32-10 keyed by seed ^ row.
+//      Two consecutive elements share one Philox call.  Local max of x.
+//   3. cutmax_core on xt (identical code to the CutMax kernel).
+//   4. token = argmax Z, all-gathered across the cluster together with x_tok
+//      and max(x) (one 32-byte record per CTA pushed to every CTA).
+//   5. One pass over x (shared memory): e = exp(x - max x), sums of e and of
+//      e over {x_k > x_tok}; one exchange; inside = above < p * total.
+// The noise is generated on chip and never stored; HBM traffic is 8n bytes
+// read per row plus 5 bytes written (+ 8n if the one-hot output is requested).
+#pragma once
+
+#include "cutmax_kernel.cuh"
+
+namespace pam {
+
+struct SamplerArgs {
+  const double* x;
+  double* onehot;  // nullable
+  int32_t* token;
+  uint8_t* inside;
+  int32_t* status;
+  int64_t ldx, ld_onehot, B, n;
+  int32_t L;
+  int32_t ctrl_offset;
+  double inv_alpha;
+  double p_nucleus;
+  uint64_t seed, draw;
+  int32_t tma;  // 1: TMA bulk load (16-byte aligned rows), 0: thread copy
+  RowParams rp;
+};
+
+template <int NT, int E, int P, bool GUMBEL>
+__global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a) {
+  constexpr int VEC = 2;
+  constexpr int NV = E / VEC;
+  constexpr int NW = NT / 32;
+  static_assert(E % VEC == 0, "E must be even");
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* buf = reinterpret_cast<double*>(smem_raw);
+  ControlBlock* cb = reinterpret_cast<ControlBlock*>(smem_raw + a.ctrl_offset);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const uint32_t C = ptx::cluster_nctarank();
+  const int64_t cid = ptx::cluster_id_x();
+  const int64_t ncl = ptx::nclusters_x();
+  const int64_t n = a.n;
+  const int64_t base = (int64_t)rank * a.L;
+  const int64_t rem = n - base;
+  const int len = rem <= 0 ? 0 : (rem < a.L ? (int)rem : a.L);
+  const double nd = (double)n;
+  const double mphantom = (double)((int64_t)C * NT * E - n);
+  const uint32_t bar_load = ptx::smem_addr(&cb->mb_load);
+  const uint32_t load_bytes = (uint32_t)len * 8u;
+  const uint64_t policy = ptx::policy_evict_first();
+
+  if (tid == 0) {
+    ptx::mbar_init(bar_load, 1);
+    ptx::mbar_init(ptx::smem_addr(&cb->mb_x[0]), 1);
+    ptx::mbar_init(ptx::smem_addr(&cb->mb_x[1]), 1);
+    ptx::mbar_init(ptx::smem_addr(&cb->mb_g), 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 16u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 16u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_g), C * 32u);
+  }
+  ptx::cluster_sync();
+
+  uint32_t xround = 0, load_par = 0, g_par = 0;
+  double v[E];
+
+  for (int64_t row = cid; row < a.B; row += ncl) {
+    const double* xrow = a.x + row * a.ldx;
+    const double K0 = __ldg(xrow);
+    __syncthreads();  // landing buffer and wred of the previous row retired
+    if (a.tma && tid == 0) {
+      ptx::mbar_arrive_expect_tx(bar_load, load_bytes);
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(xrow + base);
+      for (uint32_t off = 0; off < load_bytes; off += 32768u) {
+        const uint32_t nb = (load_bytes - off) < 32768u ? (load_bytes - off) : 32768u;
+        ptx::bulk_g2s(ptx::smem_addr(buf) + off, src + off, nb, bar_load, policy);
+      }
+    }
+    // Noise first (independent of x), then wait for the data.
+    const uint64_t key = a.seed ^ (uint64_t)row;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int li0 = (k * NT + tid) * VEC;
+      double u0, u1;
+      uniform_pair(key, a.draw, (uint64_t)(base + li0) >> 1, &u0, &u1);
+      v[k * VEC + 0] = GUMBEL ? gumbel_from_u(u0) : beta_icdf(u0, a.inv_alpha);
+      v[k * VEC + 1] = GUMBEL ? gumbel_from_u(u1) : beta_icdf(u1, a.inv_alpha);
+    }
+    if (a.tma) {
+      ptx::mbar_wait_cta(bar_load, load_par);
+      load_par ^= 1u;
+    } else {
+      for (int i = tid; i < len; i += NT) buf[i] = __ldg(xrow + base + i);
+      __syncthreads();
+    }
+    double xmax = -HUGE_VAL;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int li0 = (k * NT + tid) * VEC;
+      if (li0 + VEC <= len) {
+        const double2 t = *reinterpret_cast<const double2*>(buf + li0);
+        v[k * VEC + 0] = t.x + v[k * VEC + 0];  // Alg. 3 line 5: x~ = x + G
+        v[k * VEC + 1] = t.y + v[k * VEC + 1];
+        xmax = fmax(xmax, fmax(t.x, t.y));
+      } else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          if (li0 + j < len) {
+            const double xv = buf[li0 + j];
+            v[k * VEC + j] = xv + v[k * VEC + j];
+            xmax = fmax(xmax, xv);
+          } else {
+            v[k * VEC + j] = K0;  // phantom (see cutmax_core)
+          }
+        }
+      }
+    }
+
+    double rnorm = 1.0;
+    int st = cutmax_core<double, NT, E, P>(v, K0, mphantom, a.rp, nd, cb, xround, rank, C, nullptr, rnorm);
+
+    // token candidate over Z = Y * rnorm (and optional one-hot store)
+    double best = -HUGE_VAL, bestx = 0.0;
+    long long besti = 0x7fffffffffffffffLL;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int li0 = (k * NT + tid) * VEC;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        const double o = v[k * VEC + j] * rnorm;
+        if (li0 + j < len) {
+          if (o > best) {
+            best = o;
+            besti = base + li0 + j;
+            bestx = buf[li0 + j];
+          }
+          if (a.onehot) a.onehot[row * a.ld_onehot + base + li0 + j] = o;
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, best, off);
+      const long long oi = __shfl_down_sync(0xffffffffu, besti, off);
+      const double ox = __shfl_down_sync(0xffffffffu, bestx, off);
+      if (cand_better(ov, oi, best, besti)) { best = ov; besti = oi; bestx = ox; }
+      xmax = fmax(xmax, __shfl_down_sync(0xffffffffu, xmax, off));
+    }
+    if (lane == 0) cb->wred[warp] = make_double2(best, __longlong_as_double(besti));
+    __shared__ double2 wx[32];
+    if (lane == 0) wx[warp] = make_double2(bestx, xmax);
+    __syncthreads();
+    if (warp == 0) {
+      const double2 w = (lane < NW) ? cb->wred[lane] : make_double2(-HUGE_VAL, __longlong_as_double(0x7fffffffffffffffLL));
+      const double2 wxx = (lane < NW) ? wx[lane] : make_double2(0.0, -HUGE_VAL);
+      best = w.x;
+      besti = __double_as_longlong(w.y);
+      bestx = wxx.x;
+      xmax = wxx.y;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, best, off);
+        const long long oi = __shfl_down_sync(0xffffffffu, besti, off);
+        const double ox = __shfl_down_sync(0xffffffffu, bestx, off);
+        if (cand_better(ov, oi, best, besti)) { best = ov; besti = oi; bestx = ox; }
+        xmax = fmax(xmax, __shfl_down_sync(0xffffffffu, xmax, off));
+      }
+      best = __shfl_sync(0xffffffffu, best, 0);
+      besti = __shfl_sync(0xffffffffu, besti, 0);
+      bestx = __shfl_sync(0xffffffffu, bestx, 0);
+      xmax = __shfl_sync(0xffffffffu, xmax, 0);
+      if (lane < (int)C) {  // all-gather: 32-byte record to every CTA
+        const uint32_t bar = ptx::mapa(ptx::smem_addr(&cb->mb_g), (uint32_t)lane);
+        ptx::st_async_b64x2(ptx::mapa(ptx::smem_addr(&cb->gat[rank][0]), (uint32_t)lane),
+                            (uint64_t)__double_as_longlong(best), (uint64_t)besti, bar);
+        ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->gat[rank][1]), (uint32_t)lane), bestx, xmax, bar);
+      }
+    }
+    ptx::mbar_wait_cluster(ptx::smem_addr(&cb->mb_g), g_par);
+    g_par ^= 1u;
+    if (tid == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_g), C * 32u);  // arm next row
+    {
+      const bool have = lane < (int)C;
+      const double2 r0 = have ? cb->gat[lane][0] : make_double2(-HUGE_VAL, __longlong_as_double(0x7fffffffffffffffLL));
+      const double2 r1 = have ? cb->gat[lane][1] : make_double2(0.0, -HUGE_VAL);
+      best = r0.x;
+      besti = __double_as_longlong(r0.y);
+      bestx = r1.x;
+      xmax = r1.y;
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, best, off);
+        const long long oi = __shfl_down_sync(0xffffffffu, besti, off);
+        const double ox = __shfl_down_sync(0xffffffffu, bestx, off);
+        if (cand_better(ov, oi, best, besti)) { best = ov; besti = oi; bestx = ox; }
+        xmax = fmax(xmax, __shfl_down_sync(0xffffffffu, xmax, off));
+      }
+      besti = __shfl_sync(0xffffffffu, besti, 0);
+      bestx = __shfl_sync(0xffffffffu, bestx, 0);
+      xmax = __shfl_sync(0xffffffffu, xmax, 0);
+    }
+
+    // nucleus membership: sum over x_k > x_tok of exp(x_k - max) vs p * total
+    double tot = 0.0, above = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int li0 = (k * NT + tid) * VEC;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        if (li0 + j < len) {
+          const double xv = buf[li0 + j];
+          const double e = exp_p(xv - xmax);
+          tot += e;
+          if (xv > bestx) above += e;
+        }
+      }
+    }
+    const double2 ta = cluster_sum2<NT>(tot, above, cb, xround, rank, C);
+    if (rank == 0 && tid == 0) {
+      if (a.token) a.token[row] = (st == PAM_OK) ? (int32_t)besti : -1;
+      if (a.inside) a.inside[row] = (st == PAM_OK && ta.y < a.p_nucleus * ta.x) ? 1 : 0;
+      if (a.status) a.status[row] = st;
+    }
+  }
+  ptx::cluster_sync();
+}
+
+}  // namespace pam

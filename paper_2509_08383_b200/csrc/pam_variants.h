@@ -1,0 +1,23 @@
+// pam_variants.h — the compiled kernel instantiations the launcher can pick
+// from.  Each table lives in its own translation unit so nvcc builds them in
+// parallel.
+#pragma once
+
+namespace pam {
+
+struct Variant {
+  int elem_bytes, nt, e;
+  const void* fn[2][2];  // [P==3][TMA]
+};
+
+struct SamplerVariant {
+  int nt, e;
+  const void* fn[2][2];  // [P==3][GUMBEL]
+};
+
+extern const Variant kCutmaxVariants[];
+extern const int kNumCutmaxVariants;
+extern const SamplerVariant kSamplerVariants[];
+extern const int kNumSamplerVariants;
+
+}  // namespace pam

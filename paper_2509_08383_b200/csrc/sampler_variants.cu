@@ -1,0 +1,22 @@
+// sampler_variants.cu — instantiations of sampler_rows_kernel<NT, E, P, GUMBEL>.
+#include "nucleus_kernel.cuh"
+#include "pam_variants.h"
+
+namespace pam {
+
+#define PAM_SAMPLER_VARIANT(NT, E)                                                                             \
+  {                                                                                                            \
+    NT, E, {                                                                                                   \
+      {(const void*)sampler_rows_kernel<NT, E, 0, false>, (const void*)sampler_rows_kernel<NT, E, 0, true>},   \
+          {(const void*)sampler_rows_kernel<NT, E, 3, false>, (const void*)sampler_rows_kernel<NT, E, 3, true>} \
+    }                                                                                                          \
+  }
+
+const SamplerVariant kSamplerVariants[] = {
+    PAM_SAMPLER_VARIANT(64, 2),   PAM_SAMPLER_VARIANT(128, 8),  PAM_SAMPLER_VARIANT(256, 8),
+    PAM_SAMPLER_VARIANT(256, 16), PAM_SAMPLER_VARIANT(512, 16), PAM_SAMPLER_VARIANT(512, 24),
+    PAM_SAMPLER_VARIANT(512, 38),
+};
+const int kNumSamplerVariants = sizeof(kSamplerVariants) / sizeof(kSamplerVariants[0]);
+
+}  // namespace pam

@@ -1,0 +1,388 @@
+"""Python host mirror of the reference's `polyargmax` interface for the CutMax
+decoding core (SPEC.md modules `core`, `polyapprox` scalars, `sampling`).
+
+Same operation names, argument meaning and error behaviour as the SPEC:
+
+    cutmax(x, params)                      SPEC.md:60-69   -> ScoreVector
+    cutmaxStep(y, p, c)                    SPEC.md:71-79   -> (next, ResidualStats)
+    goldschmidtInv(x, cfg)
+    goldschmidtInvSqrt(x, cfg)
+    gumbelFromUniform(u)
+    gumbelMaxSample(x, params, seed)
+    betaInverseCdf(u, alpha)
+    nucleusAlpha(p, q)
+    nucleusOneShotSample(x, cfg, params)
+
+plus batched forms over host arrays (numpy) and device tensors (torch, CUDA).
+Every vector operation runs in libpam.so's sm_100a kernels; nothing here
+computes on the CPU except argument marshalling.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence, Union
+
+import numpy as np
+
+from . import _abi
+from .errors import DomainError, InvalidParamsError, raise_for_status
+
+_lib = _abi.load()
+
+# ---------------------------------------------------------------- types ----
+
+
+@dataclass
+class ApproxConfig:
+    """ApproxConfig.  rescale: 'auto' | 'static' | 'none'."""
+
+    iterations: int = 5
+    lo: float = 0.25
+    hi: float = 1.0
+    alphaBits: int = 7
+    rescale: str = "auto"
+    scaleLog2: int = 0
+
+    @staticmethod
+    def invsqrtPreset(alphaBits: int = 7) -> "ApproxConfig":
+        """Table 3: invsqrt iterations 5/6/7/8 for alpha 7/9/11/13."""
+        it = 5 if alphaBits <= 7 else 6 if alphaBits <= 9 else 7 if alphaBits <= 11 else 8
+        return ApproxConfig(iterations=it, lo=0.25, hi=1.0, alphaBits=alphaBits)
+
+    @staticmethod
+    def invPreset(alphaBits: int = 7) -> "ApproxConfig":
+        d = 0
+        while (1 << (d + 1)) < alphaBits + 1:
+            d += 1
+        return ApproxConfig(iterations=max(d, 2), lo=0.5, hi=1.0, alphaBits=alphaBits)
+
+    def lower(self) -> _abi.pam_approx_config:
+        r = _abi.pam_approx_config()
+        r.iterations = int(self.iterations)
+        r.alpha_bits = int(self.alphaBits)
+        r.rescale = {"auto": _abi.PAM_RESCALE_AUTO, "static": _abi.PAM_RESCALE_STATIC,
+                     "none": _abi.PAM_RESCALE_NONE}[self.rescale]
+        r.scale_log2 = int(self.scaleLog2)
+        r.lo = float(self.lo)
+        r.hi = float(self.hi)
+        return r
+
+
+def _sched(v, T, name):
+    if isinstance(v, (int, float, np.integer, np.floating)):
+        return [v] * T
+    v = list(v)
+    if len(v) == 1:
+        return v * T
+    if len(v) != T:
+        raise InvalidParamsError(f"{name} schedule must have length 1 or T (SPEC.md:124)")
+    return v
+
+
+@dataclass
+class CutMaxParams:
+    """CutMaxParams: p odd >= 3, c > 0, T >= 1; scalars broadcast."""
+
+    p: Union[int, Sequence[int]] = 3
+    c: Union[float, Sequence[float]] = 5.0
+    T: int = 4
+    checked: bool = True
+    guarantee: bool = False
+    normalize: bool = True
+    epsVar: float = 1e-24
+    epsStop: float = 0.0
+    invsqrtMode: str = "exact"  # 'exact' | 'poly'
+    invMode: str = "exact"
+    invsqrt: Union[ApproxConfig, Sequence[ApproxConfig]] = field(default_factory=ApproxConfig.invsqrtPreset)
+    inv: ApproxConfig = field(default_factory=ApproxConfig.invPreset)
+
+    def lower(self) -> _abi.pam_cutmax_params:
+        T = int(self.T)
+        if T < 1 or T > _abi.PAM_MAX_T:
+            raise InvalidParamsError("T must be in [1, 16] (SPEC.md:67: T=0 is invalid)")
+        r = _abi.pam_cutmax_params()
+        _lib.pam_default_params(C.byref(r), T, 3, 5.0)
+        r.flags = ((0 if self.checked else _abi.PAM_F_UNCHECKED) | (_abi.PAM_F_GUARANTEE if self.guarantee else 0)
+                   | (0 if self.normalize else _abi.PAM_F_NO_NORMALIZE))
+        r.eps_var = float(self.epsVar)
+        r.eps_stop = float(self.epsStop)
+        r.invsqrt_mode = {"exact": _abi.PAM_MODE_EXACT, "poly": _abi.PAM_MODE_POLY}[self.invsqrtMode]
+        r.inv_mode = {"exact": _abi.PAM_MODE_EXACT, "poly": _abi.PAM_MODE_POLY}[self.invMode]
+        ps = _sched(self.p, T, "p")
+        cs = _sched(self.c, T, "c")
+        inv = [self.invsqrt] if isinstance(self.invsqrt, ApproxConfig) else list(self.invsqrt)
+        inv = _sched(inv, T, "invsqrt") if len(inv) != 1 else inv * T
+        for t in range(T):
+            r.p[t] = int(ps[t])
+            r.c[t] = float(cs[t])
+            r.invsqrt[t] = inv[t].lower()
+        r.inv = self.inv.lower()
+        return r
+
+
+@dataclass
+class ScoreVector:
+    """ScoreVector plus the argmax computed by the kernel."""
+
+    values: np.ndarray
+    normalized: bool
+    argmax: int
+
+
+@dataclass
+class ResidualStats:
+    """ResidualStats."""
+
+    mu: float
+    s2: float
+    residuals: np.ndarray
+    dispersion: float
+
+
+@dataclass
+class SamplerConfig:
+    """SamplerConfig; alpha <= 0 derives ln(1-q)/ln(p)."""
+
+    p: float = 0.9
+    q: Optional[float] = None
+    alpha: float = 0.0
+    seed: int = 0
+    draw: int = 0
+
+    def lower(self) -> _abi.pam_sampler_cfg:
+        r = _abi.pam_sampler_cfg()
+        r.p = float(self.p)
+        r.q = float(self.p if self.q is None else self.q)
+        r.alpha = float(self.alpha)
+        r.seed = int(self.seed) & 0xFFFFFFFFFFFFFFFF
+        r.draw = int(self.draw) & 0xFFFFFFFFFFFFFFFF
+        return r
+
+
+@dataclass
+class SampleOutcome:
+    """SampleOutcome."""
+
+    onehot: np.ndarray
+    tokenIndex: int
+    insideNucleus: bool
+
+
+# ---------------------------------------------------------------- scalars --
+
+
+def goldschmidtInv(x: float, cfg: Optional[ApproxConfig] = None) -> float:
+    cfg = cfg or ApproxConfig(iterations=5, lo=1e-300, hi=2.0, rescale="none")
+    out = C.c_double()
+    c = cfg.lower()
+    raise_for_status(_lib.pam_goldschmidt_inv(float(x), C.byref(c), C.byref(out)), what="goldschmidtInv")
+    return out.value
+
+
+def goldschmidtInvSqrt(x: float, cfg: Optional[ApproxConfig] = None) -> float:
+    cfg = cfg or ApproxConfig(iterations=5, lo=1e-300, hi=2.0, rescale="none")
+    out = C.c_double()
+    c = cfg.lower()
+    raise_for_status(_lib.pam_goldschmidt_invsqrt(float(x), C.byref(c), C.byref(out)), what="goldschmidtInvSqrt")
+    return out.value
+
+
+def nucleusAlpha(p: float, q: Optional[float] = None) -> float:
+    out = C.c_double()
+    raise_for_status(_lib.pam_nucleus_alpha(float(p), float(p if q is None else q), C.byref(out)),
+                     what="nucleusAlpha")
+    return out.value
+
+
+def betaInverseCdf(u: float, alpha: float) -> float:
+    if not (0.0 <= u <= 1.0) or not (alpha > 0.0):
+        raise DomainError("betaInverseCdf needs u in [0,1] and alpha > 0")
+    return _lib.pam_beta_inverse_cdf(float(u), float(alpha))
+
+
+def gumbelFromUniform(u: float) -> float:
+    out = C.c_double()
+    raise_for_status(_lib.pam_gumbel_from_uniform(float(u), C.byref(out)), what="gumbelFromUniform")
+    return out.value
+
+
+def uniform(seed: int, row: int, draw: int, index: int) -> float:
+    """The pinned Philox4x32-10 uniform for (seed, row, draw, element index)."""
+    m = 0xFFFFFFFFFFFFFFFF
+    return _lib.pam_uniform(seed & m, row & m, draw & m, index & m)
+
+
+# ----------------------------------------------------- host-array batch API
+
+
+def _as_rows(x, dtype):
+    a = np.ascontiguousarray(np.asarray(x, dtype=dtype))
+    if a.ndim == 1:
+        a = a[None, :]
+    if a.ndim != 2:
+        raise InvalidParamsError("expected a vector or a (B, n) matrix")
+    return a
+
+
+def cutmax_batch(X, params: Optional[CutMaxParams] = None, raise_on_error: bool = True):
+    """Batched CutMax over host rows (float64 or float32): returns (Z, argmax, status).
+
+    Host -> device copies, the fused kernel and device -> host copies all happen
+    inside the library call (pam_cutmax_batch_host_*)."""
+    params = params or CutMaxParams()
+    dtype = np.float32 if np.asarray(X).dtype == np.float32 else np.float64
+    a = _as_rows(X, dtype)
+    B, n = a.shape
+    z = np.empty_like(a)
+    am = np.empty(B, dtype=np.int32)
+    st = np.empty(B, dtype=np.int32)
+    prm = params.lower()
+    fn = _lib.pam_cutmax_batch_host_f32 if dtype == np.float32 else _lib.pam_cutmax_batch_host_f64
+    rc = fn(a.ctypes.data, B, n, C.byref(prm), z.ctypes.data, am.ctypes.data, st.ctypes.data)
+    raise_for_status(rc, what="cutmax_batch")
+    if raise_on_error:
+        bad = np.nonzero(st & 0xFF)[0]
+        if len(bad):
+            raise_for_status(int(st[bad[0]]), row=int(bad[0]))
+    return z, am, st
+
+
+def cutmax(x, params: Optional[CutMaxParams] = None) -> ScoreVector:
+    """cutmax(x, params) -> ScoreVector."""
+    params = params or CutMaxParams()
+    z, am, _ = cutmax_batch(np.asarray(x, dtype=np.float64)[None, :], params)
+    return ScoreVector(values=z[0], normalized=params.normalize, argmax=int(am[0]))
+
+
+# --------------------------------------------------------- device API ------
+
+
+def _torch():
+    import torch  # plumbing only: device memory and streams
+
+    return torch
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def cutmax_batch_device(x, params: Optional[CutMaxParams] = None, z=None, argmax=None, status=None,
+                        stats=None, stream=None):
+    """Batched CutMax on a CUDA tensor (B, n) float64/float32, stream-ordered.
+
+    Returns (z, argmax, status) device tensors.  ``stats`` (optional float64
+    tensor (B, T, 2)) receives {mu_t, s2_t}.  Raises only for invalid params or
+    launch failures; data-dependent failures land in ``status``."""
+    torch = _torch()
+    params = params or CutMaxParams()
+    if x.dim() != 2 or not x.is_cuda:
+        raise InvalidParamsError("x must be a 2-D CUDA tensor")
+    B, n = x.shape
+    ld = x.stride(0)
+    if x.stride(1) != 1:
+        raise InvalidParamsError("rows must be contiguous")
+    if z is None:
+        z = torch.empty((B, n), dtype=x.dtype, device=x.device)
+    if argmax is None:
+        argmax = torch.empty(B, dtype=torch.int32, device=x.device)
+    if status is None:
+        status = torch.empty(B, dtype=torch.int32, device=x.device)
+    prm = params.lower()
+    if x.dtype == torch.float64:
+        fn = _lib.pam_cutmax_batch_f64
+    elif x.dtype == torch.float32:
+        fn = _lib.pam_cutmax_batch_f32
+    else:
+        raise InvalidParamsError("dtype must be float64 or float32")
+    rc = fn(x.data_ptr(), ld, B, n, C.byref(prm), z.data_ptr(), z.stride(0), argmax.data_ptr(),
+            status.data_ptr(), stats.data_ptr() if stats is not None else None, _stream_ptr(stream))
+    raise_for_status(rc, what="cutmax_batch_device")
+    return z, argmax, status
+
+
+def _sample_device(fn_name, x, cfg: SamplerConfig, params: CutMaxParams, onehot=None, stream=None):
+    torch = _torch()
+    if x.dim() != 2 or not x.is_cuda or x.dtype != torch.float64:
+        raise InvalidParamsError("x must be a 2-D float64 CUDA tensor")
+    B, n = x.shape
+    token = torch.empty(B, dtype=torch.int32, device=x.device)
+    inside = torch.empty(B, dtype=torch.uint8, device=x.device)
+    status = torch.empty(B, dtype=torch.int32, device=x.device)
+    c = cfg.lower()
+    prm = params.lower()
+    rc = getattr(_lib, fn_name)(x.data_ptr(), x.stride(0), B, n, C.byref(c), C.byref(prm), token.data_ptr(),
+                                inside.data_ptr(), onehot.data_ptr() if onehot is not None else None,
+                                onehot.stride(0) if onehot is not None else 0, status.data_ptr(),
+                                _stream_ptr(stream))
+    raise_for_status(rc, what=fn_name)
+    return token, inside, status
+
+
+def nucleus_sample_batch_device(x, cfg: SamplerConfig, params: Optional[CutMaxParams] = None, onehot=None,
+                                stream=None):
+    """Fused Beta-cut nucleus sampling (Alg. 3) over CUDA rows; returns (token, inside, status)."""
+    return _sample_device("pam_nucleus_sample_batch_f64", x, cfg, params or CutMaxParams(), onehot, stream)
+
+
+def gumbel_sample_batch_device(x, cfg: SamplerConfig, params: Optional[CutMaxParams] = None, onehot=None,
+                               stream=None):
+    """Fused Gumbel-max sampling (Lemma 1) over CUDA rows; inside[] against nucleus mass cfg.p."""
+    return _sample_device("pam_gumbel_sample_batch_f64", x, cfg, params or CutMaxParams(), onehot, stream)
+
+
+def _one_row_sample(fn, x, cfg, params, row_index):
+    torch = _torch()
+    xv = torch.as_tensor(np.asarray(x, dtype=np.float64), device="cuda")[None, :]
+    oh = torch.empty_like(xv)
+    c2 = SamplerConfig(p=cfg.p, q=cfg.q, alpha=cfg.alpha, seed=(cfg.seed ^ row_index), draw=cfg.draw)
+    tok, ins, st = fn(xv, c2, params, onehot=oh)
+    s = int(st.item())
+    raise_for_status(s, row=0)
+    return SampleOutcome(onehot=oh[0].cpu().numpy(), tokenIndex=int(tok.item()), insideNucleus=bool(ins.item()))
+
+
+def nucleusOneShotSample(x, cfg: SamplerConfig, params: Optional[CutMaxParams] = None,
+                         row_index: int = 0) -> SampleOutcome:
+    """nucleusOneShotSample: noise keyed by cfg.seed ^ row_index."""
+    return _one_row_sample(nucleus_sample_batch_device, x, cfg, params or CutMaxParams(), row_index)
+
+
+def gumbelMaxSample(x, params: Optional[CutMaxParams] = None, seed: int = 0, nucleus_p: float = 0.9) -> SampleOutcome:
+    """gumbelMaxSample."""
+    return _one_row_sample(gumbel_sample_batch_device, x, SamplerConfig(p=nucleus_p, seed=seed),
+                           params or CutMaxParams(), 0)
+
+
+def cutmaxStep(y, p: int, c: float, epsVar: float = 1e-24):
+    """cutmaxStep: next_i = (1 + r_i/c)^p on the GPU (T=1,
+    un-normalised), with mu/s2 from the kernel's stats output.  Residuals and
+    the non-top dispersion are derived from those stats."""
+    torch = _torch()
+    yv = torch.as_tensor(np.asarray(y, dtype=np.float64), device="cuda")[None, :]
+    prm = CutMaxParams(p=p, c=c, T=1, checked=False, normalize=False, epsVar=epsVar)
+    stats = torch.empty((1, 1, 2), dtype=torch.float64, device="cuda")
+    z, _, st = cutmax_batch_device(yv, prm, stats=stats)
+    raise_for_status(int(st.item()))
+    mu, s2 = (float(v) for v in stats[0, 0].cpu().numpy())
+    yh = np.asarray(y, dtype=np.float64)
+    r = (yh - mu) * (1.0 / np.sqrt(s2))
+    top = int(np.argmax(yh))
+    nt = np.delete(r, top)
+    disp = float(((nt - nt.mean()) ** 2).sum())
+    return z[0].cpu().numpy(), ResidualStats(mu=mu, s2=s2, residuals=r, dispersion=disp)
+
+
+def launch_info(dtype_bytes: int, B: int, n: int, params: Optional[CutMaxParams] = None) -> dict:
+    """Launch geometry the library picks for (dtype, B, n) (needs a GPU)."""
+    info = _abi.pam_launch_info()
+    prm = (params or CutMaxParams()).lower()
+    raise_for_status(_lib.pam_query_launch(dtype_bytes, B, n, C.byref(prm), C.byref(info)))
+    return {k: getattr(info, k) for k, _ in info._fields_}
+
+
+def kernel_launch_count() -> int:
+    return int(_lib.pam_kernel_launch_count())

@@ -1,0 +1,154 @@
+"""CPU: the C-ABI library loads, exports every symbol include/pam_c_api.h
+declares, and its host-side logic (parameter validation, defaults, scalar API,
+error mapping) behaves like the reference interface.  No kernel launches."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pam_c_api.h")
+LIB = os.path.join(ROOT, "paper_2509_08383_b200", "libpam.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pam_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_expected_entry_points():
+    fns = declared_functions()
+    for f in ("pam_cutmax_batch_f64", "pam_cutmax_batch_f32", "pam_cutmax_batch_host_f64",
+              "pam_nucleus_sample_batch_f64", "pam_gumbel_sample_batch_f64", "pam_goldschmidt_inv",
+              "pam_goldschmidt_invsqrt", "pam_nucleus_alpha", "pam_beta_inverse_cdf"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(pam):
+    lib = C.CDLL(LIB)
+    missing = [f for f in declared_functions() if not hasattr(lib, f)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (pam_\w+)", out))
+    assert set(declared_functions()) <= exported
+    # the Python mirror binds every declared function with a signature
+    from paper_2509_08383_b200 import _abi
+    assert set(declared_functions()) == set(_abi.SIGNATURES)
+
+
+def test_library_is_sm100a_native():
+    out = subprocess.run(["cuobjdump", "-lelf", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
+    for mnemonic in ("UBLKCP", "STAS", "SYNCS", "DFMA"):  # TMA bulk copy, DSMEM push, mbarrier, fp64
+        assert mnemonic in sass, mnemonic
+
+
+def test_abi_version_and_status_strings(pam):
+    from paper_2509_08383_b200 import _abi
+    lib = _abi.load()
+    assert lib.pam_abi_version() == 1
+    assert lib.pam_status_string(0) == b"ok"
+    assert b"degenerate" in lib.pam_status_string(2)
+    assert lib.pam_status_string(2 | 0x100) == lib.pam_status_string(2)  # flag bits ignored
+
+
+def test_param_validation(pam):
+    from paper_2509_08383_b200 import _abi
+    lib = _abi.load()
+
+    def v(n=100, **kw):
+        return lib.pam_validate_cutmax_params(C.byref(pam.CutMaxParams(**kw).lower()), n)
+
+    assert v() == 0
+    assert v(n=1) == 1                                   # n >= 2
+    assert v(p=4) == 1 and v(p=4, checked=False) == 0    # even p only unchecked
+    assert v(p=1) == 1
+    assert v(c=0.0) == 1 and v(c=-1.0) == 1             # c > 0
+    assert v(c=5.0, guarantee=True, n=100) == 1          # c > sqrt(n-1)
+    assert v(c=10.0, guarantee=True, n=100) == 0
+    prm = pam.CutMaxParams().lower()
+    prm.T = 0
+    assert lib.pam_validate_cutmax_params(C.byref(prm), 10) == 1  # T=0 invalid
+    with pytest.raises(pam.InvalidParamsError):
+        pam.CutMaxParams(T=0).lower()
+    with pytest.raises(pam.InvalidParamsError):
+        pam.CutMaxParams(T=4, p=[3, 3]).lower()          # schedule length 1 or T
+
+
+def test_schedule_broadcast(pam):
+    prm = pam.CutMaxParams(p=5, c=7.0, T=3).lower()
+    assert list(prm.p[:3]) == [5, 5, 5] and list(prm.c[:3]) == [7.0, 7.0, 7.0]
+    prm = pam.CutMaxParams(p=[16, 4, 4, 6], c=[5, 3, 3, 3], T=4, checked=False).lower()
+    assert list(prm.p[:4]) == [16, 4, 4, 6] and prm.flags & 1
+
+
+def test_host_scalars_match_oracle_bit_for_bit(pam, orc):
+    rng = np.random.default_rng(0)
+    cfg_inv = pam.ApproxConfig(iterations=5, lo=1e-300, hi=2.0, rescale="none")
+    for x in rng.uniform(0.01, 1.99, 500):
+        assert pam.goldschmidtInv(x, cfg_inv) == orc.scalar("goldschmidt_inv", x, 5)
+        assert pam.goldschmidtInvSqrt(x, cfg_inv) == orc.scalar("invsqrt_newton", x, 5)
+    auto = pam.ApproxConfig(iterations=6)
+    for x in 10.0 ** rng.uniform(-30, 30, 500):
+        assert pam.goldschmidtInvSqrt(x, auto) == orc.approx_cfg(x, auto.lower(), inv=False)[1]
+        assert pam.goldschmidtInv(x, auto) == orc.approx_cfg(x, auto.lower(), inv=True)[1]
+    for u in rng.uniform(0, 1, 500):
+        assert pam.betaInverseCdf(u, 21.854345326782838) == orc.scalar("beta_icdf", u, 21.854345326782838)
+        assert pam.gumbelFromUniform(u) == orc.scalar("gumbel", u)
+    for i in range(300):
+        assert pam.uniform(2**63 + 5, 17, 3, i) == orc.scalar("uniform", 2**63 + 5, 17, 3, i)
+    assert pam.nucleusAlpha(0.9) == orc.scalar("nucleus_alpha", 0.9, 0.9)
+
+
+def test_scalar_errors(pam):
+    with pytest.raises(pam.RangeError):
+        pam.goldschmidtInv(2.5)
+    with pytest.raises(pam.DomainError):
+        pam.gumbelFromUniform(0.0)
+    with pytest.raises(pam.DomainError):
+        pam.nucleusAlpha(1.0, 0.5)
+    with pytest.raises(pam.DomainError):
+        pam.betaInverseCdf(1.5, 2.0)
+    assert pam.goldschmidtInv(1.0) == 1.0 and pam.goldschmidtInvSqrt(1.0) == 1.0
+
+
+def test_error_hierarchy_matches_reference_names(pam):
+    from paper_2509_08383_b200 import errors
+    for name in ("Error", "DegenerateInputError", "InvalidParamsError", "RangeError", "DomainError",
+                 "NonFiniteError"):
+        cls = getattr(errors, name)
+        assert issubclass(cls, errors.Error)
+    e = errors.NonFiniteError("bad", 7)
+    assert e.vector_index == 7 and "vector 7" in str(e)
+    hdr = open(os.path.join(ROOT, "include", "polyargmax", "errors.hpp")).read()
+    for name in ("DegenerateInputError", "InvalidParamsError", "RangeError", "DomainError", "WidthMismatchError",
+                 "BadRotationError", "RangeProofViolation", "SingularityError", "BadSpecError", "FormatError",
+                 "NonFiniteError"):
+        assert name in hdr
+
+
+def test_cpp_api_header_compiles():
+    """The drop-in C++ API header builds standalone with the reference's C++20 setting."""
+    src = '#include "polyargmax/polyargmax.hpp"\nint main(){ polyargmax::CutMaxParams p; auto l = p.lower(); return l.T == 4 ? 0 : 1; }\n'
+    tmp = "/tmp/pam_hdr_test.cpp"
+    open(tmp, "w").write(src)
+    r = subprocess.run(["/usr/bin/g++", "-std=c++20", "-Wall", "-Wextra", "-fsyntax-only",
+                        "-I", os.path.join(ROOT, "include"), tmp], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+def test_no_oracle_in_product():
+    """The product never imports or links the oracle."""
+    pkg = os.path.join(ROOT, "paper_2509_08383_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"(#|//).*", "", txt).replace('"""', ""), f
+    out = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout
+    assert "oracle" not in out
