@@ -175,13 +175,16 @@ int pam_gumbel_sample_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int6
 
 /* ---- introspection (bench / tests) --------------------------------------- */
 typedef struct pam_launch_info {
-  int32_t threads, elems_per_thread, cluster, clusters, ctas, smem_bytes, tma, kernel_id;
+  int32_t threads, elems_per_thread, cluster, clusters, ctas, smem_bytes, tma, kernel_id, groups;
 } pam_launch_info;
 /* Launch geometry the library would use for (dtype_bytes, B, n). */
 int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_params* prm,
                      pam_launch_info* info);
 /* Number of kernels this library launched since load (tests / bench evidence). */
 int64_t pam_kernel_launch_count(void);
+/* Debug: device buffer (grid x 8 rows x 32 events of int64 clock64 stamps) that
+ * the CutMax kernel fills with per-CTA phase timestamps; NULL disables. */
+void pam_set_trace_buffer(long long* d_buf, int64_t entries);
 /* Last CUDA error string seen by the library (thread-unsafe diagnostic). */
 const char* pam_last_cuda_error(void);
 

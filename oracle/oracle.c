@@ -284,25 +284,26 @@ int orc_cutmax(const double* x, int64_t n, const pam_cutmax_params* prm,
     }
   }
   if (iters_run) *iters_run = ran;
+  /* argmax of the final iterate Y^(T+1) (pin A7): equal to argmax Z for the
+   * positive normaliser required below, without the spurious ties the
+   * rounding of Y*inv(sum Y) can create.  Lowest index among maxima. */
+  int64_t best = 0;
+  for (i = 1; i < n; ++i) if (z[i] > z[best]) best = i;
   double total = 0.0;
   for (i = 0; i < n; ++i) total += z[i];
   if (!isfinite(total)) return PAM_ERR_RANGE;
   if (!(prm->flags & PAM_F_NO_NORMALIZE)) {
     double r;
+    if (!(total > 0.0)) return PAM_ERR_RANGE;                   /* Z must be a distribution */
     if (prm->inv_mode == PAM_MODE_POLY) {
       int rs = orc_inv_cfg(total, &prm->inv, &r);
       if (rs) return rs;
     } else {
-      if (total == 0.0) return PAM_ERR_RANGE;
       r = 1.0 / total;
     }
     for (i = 0; i < n; ++i) z[i] = z[i] * r;                    /* PAPER.md:69 / :163 */
   }
-  if (argmax) {
-    int64_t best = 0;
-    for (i = 1; i < n; ++i) if (z[i] > z[best]) best = i;      /* lowest index among maxima */
-    *argmax = (int32_t)best;
-  }
+  if (argmax) *argmax = (int32_t)best;
   return PAM_OK;
 }
 
@@ -343,26 +344,24 @@ int orc_cutmax_f32(const float* x, int64_t n, const pam_cutmax_params* prm,
       z[i] = orc_ipowf(u, p);
     }
   }
+  int64_t best = 0;
+  for (i = 1; i < n; ++i) if (z[i] > z[best]) best = i;        /* argmax of Y^(T+1), pin A7 */
   double total = 0.0;
   for (i = 0; i < n; ++i) total += (double)z[i];
   if (!isfinite(total)) return PAM_ERR_RANGE;
   if (!(prm->flags & PAM_F_NO_NORMALIZE)) {
     double r;
+    if (!(total > 0.0)) return PAM_ERR_RANGE;
     if (prm->inv_mode == PAM_MODE_POLY) {
       int rs = orc_inv_cfg(total, &prm->inv, &r);
       if (rs) return rs;
     } else {
-      if (total == 0.0) return PAM_ERR_RANGE;
       r = 1.0 / total;
     }
     float rf = (float)r;
     for (i = 0; i < n; ++i) z[i] = z[i] * rf;
   }
-  if (argmax) {
-    int64_t best = 0;
-    for (i = 1; i < n; ++i) if (z[i] > z[best]) best = i;
-    *argmax = (int32_t)best;
-  }
+  if (argmax) *argmax = (int32_t)best;
   return PAM_OK;
 }
 

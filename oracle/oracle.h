@@ -23,7 +23,9 @@
  *   A4  rescale identity invsqrt(x/b)/sqrt(b)
  *   A5  per-row key seed ^ row driving a Philox4x32-10 per-element stream
  *   A6  portable exp/log (restated here independently of the product header)
- *   A7  argmax ties -> lowest index; TieWarning when top-2 gap < 1e-9
+ *   A7  argmax of the final iterate Y^(T+1) (= argmax Z, the normaliser being
+ *       required positive: sum Y <= 0 is a RangeError), ties -> lowest index;
+ *       TieWarning when the input top-2 gap < 1e-9
  *   A9  nucleus: inside(tok) <=> sum_{x_k > x_tok} softmax(x)_k < p
  *   final normalisation uses the state after the T-th update (PAPER.md:69
  *   writes Y^(T); with Y^(1)=X that is read as the last iterate) and is

@@ -65,7 +65,8 @@ class pam_sampler_cfg(C.Structure):
 
 class pam_launch_info(C.Structure):
     _fields_ = [(k, C.c_int32) for k in
-                ("threads", "elems_per_thread", "cluster", "clusters", "ctas", "smem_bytes", "tma", "kernel_id")]
+                ("threads", "elems_per_thread", "cluster", "clusters", "ctas", "smem_bytes", "tma", "kernel_id",
+                 "groups")]
 
 
 _P = C.c_void_p
@@ -94,6 +95,7 @@ SIGNATURES = {
     "pam_query_launch": (C.c_int, [C.c_int, _I64, _I64, C.POINTER(pam_cutmax_params), C.POINTER(pam_launch_info)]),
     "pam_kernel_launch_count": (C.c_int64, []),
     "pam_last_cuda_error": (C.c_char_p, []),
+    "pam_set_trace_buffer": (None, [_P, _I64]),
 }
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))

@@ -3,11 +3,15 @@
 // Replaces core.cutmax / core.cutmaxStep (Alg. 1).
 //
 // Geometry.  One logit row is owned by one thread-block cluster of C CTAs
-// (C = 1..16).  CTA `rank` owns the contiguous slice [rank*L, min(n,(rank+1)*L))
-// and each thread keeps E elements of it in registers for all T iterations:
-// HBM is read once (1-D TMA bulk copy into a shared-memory landing buffer,
-// prefetched one row ahead) and written once (128-bit streaming stores).
-// Clusters are persistent and stride over rows.
+// (C = 1..16).  CTA `rank` owns the contiguous slice [rank*L, min(n,(rank+1)*L)).
+// A CTA runs G independent "row groups" of NTG threads each (named barriers
+// 1..G, own mbarriers, own landing buffer): group g of cluster c processes rows
+// c*G + g, c*G + g + ncl*G, ...  While one group sits in a cluster exchange or
+// streams its Z out, the other group's fp64 passes keep the SM busy.
+// Each thread of a group keeps E elements of its slice in registers for all T
+// iterations: HBM is read once (1-D TMA bulk copy into the group's shared
+// memory landing buffer, prefetched one row ahead) and written once (128-bit
+// streaming stores).
 //
 // Reductions.  Every iteration needs the row mean and variance.  Values are
 // stored shifted, v = y - K, with a shift K shared by every CTA (K = x[0] for
@@ -19,11 +23,12 @@
 // the kernel does an exact second pass sum((v-dm)^2) and a second exchange;
 // the decision is cluster-uniform because every CTA holds identical sums.
 //
-// Exchange.  warp shuffle tree -> CTA partial -> each CTA pushes its (S,Q)
-// partial into every CTA's slot array with st.async (DSMEM) completing on the
-// destination's mbarrier; every warp then sums the C partials in a fixed tree
-// order, so all CTAs compute bit-identical mu and s2.  The argmax candidate is
-// gathered to rank 0 the same way.
+// Exchange.  Each warp butterfly-reduces its lanes and pushes its partial into
+// slot (rank, warp) of every CTA of the cluster with st.async (DSMEM),
+// completing on the destination group's mbarrier; every warp then sums the
+// same C*NW slots in the same order.  xor-butterflies leave bit-identical sums
+// in every lane (IEEE addition is commutative), so all CTAs compute identical
+// mu and s2 without a broadcast.  The argmax candidate is gathered to rank 0.
 //
 // Element update (z = (y-mu)/(c sigma) + 1, y' = z^p):
 //     z = fma(v, k, b)  with k = inv_sigma/c, b = 1 - dm*k
@@ -59,21 +64,41 @@ struct CutmaxArgs {
   int32_t* status;
   double* stats;
   int64_t ldx, ldz, B, n;
-  int32_t L;            // slice length per CTA (elements)
-  int32_t ctrl_offset;  // byte offset of the control block in dynamic smem
+  int32_t L;             // slice length per CTA (elements)
+  int32_t buf_bytes;     // landing-buffer bytes per group (0 without TMA)
+  int32_t ctrl_offset;   // byte offset of the first group's control block
+  int32_t tma;           // 1: TMA bulk loads + 128-bit stores (16-byte aligned rows), 0: scalar path
+  double inv_n;          // 1/n
+  long long* trace;      // debug: per-CTA phase timestamps (pam_set_trace_buffer), normally null
+  int64_t stagger;       // start offset (SM cycles) spread over clusters / groups to de-phase them
+  int32_t debug_flags;   // dev experiments: 1 = skip Z stores
   RowParams rp;
 };
 
+// One 32-byte exchange record per (cluster rank): partial sums (a, b) and an
+// argmax candidate (value, index) used by the last exchange of a row.
+struct __align__(16) XchRecord {
+  double2 ab;
+  double2 cand;  // (value, index bits)
+};
+
 struct __align__(16) ControlBlock {
-  double2 xch[2][16];  // exchange slots, double-buffered by round parity
-  double2 cand[16];    // argmax candidates (rank 0 only)
-  double2 wred[32];    // per-warp partials
-  double2 gat[16][2];  // all-gather records (sampler: token candidate + max x)
+  XchRecord xch[2][16];  // exchange slots per cluster rank, double-buffered by round parity
+  double2 wred[32];      // per-warp partial sums (CTA pre-reduction; sampler token gather)
+  double2 wcand[32];     // per-warp argmax candidates
+  double2 gat[16][2];    // all-gather records (sampler: token candidate + max x)
   unsigned long long mb_load;
   unsigned long long mb_x[2];
-  unsigned long long mb_a;
   unsigned long long mb_g;
 };
+
+// Debug phase tracing: thread 0 of group 0 of each CTA stamps clock64() at
+// phase boundaries of its first kTraceRows rows (tools/trace.py reads them).
+constexpr int kTraceRows = 8, kTraceEvents = 32;
+#define PAM_TRACE(tr, k)                                   \
+  do {                                                     \
+    if ((tr) != nullptr && gtid == 0) (tr)[k] = clock64(); \
+  } while (0)
 
 template <typename T>
 struct ElemTraits;
@@ -93,56 +118,120 @@ __device__ __forceinline__ float fma_e(float a, float b, float c) { return fmaf(
 __device__ __forceinline__ double ipow_e(double z, int p) { return ipow(z, p); }
 __device__ __forceinline__ float ipow_e(float z, int p) { return ipowf(z, p); }
 
-// ---------------------------------------------------------------------------
-// Cluster-wide sum of two doubles.  All threads of the CTA must call it.
-template <int NT>
-__device__ __forceinline__ double2 cluster_sum2(double a, double b, ControlBlock* cb, uint32_t& round,
-                                                uint32_t rank, uint32_t C) {
-  constexpr int NW = NT / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Named barrier for the NTG threads of group g (barrier 0 is __syncthreads).
+template <int NTG>
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(NTG) : "memory");
+}
+
+__device__ __forceinline__ void butterfly_sum2(double& a, double& b) {
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    a += __shfl_down_sync(0xffffffffu, a, off);
-    b += __shfl_down_sync(0xffffffffu, b, off);
+  for (int m = 16; m > 0; m >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, m);
+    b += __shfl_xor_sync(0xffffffffu, b, m);
   }
-  if (lane == 0) cb->wred[warp] = make_double2(a, b);
-  __syncthreads();
-  const uint32_t par = round & 1u, ph = (round >> 1) & 1u;
-  if (warp == 0) {
-    double2 w = (lane < NW) ? cb->wred[lane] : make_double2(0.0, 0.0);
-    a = w.x;
-    b = w.y;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      a += __shfl_down_sync(0xffffffffu, a, off);
-      b += __shfl_down_sync(0xffffffffu, b, off);
-    }
-    a = __shfl_sync(0xffffffffu, a, 0);
-    b = __shfl_sync(0xffffffffu, b, 0);
-    if (lane < (int)C) {
-      const uint32_t dst = ptx::mapa(ptx::smem_addr(&cb->xch[par][rank]), (uint32_t)lane);
-      const uint32_t bar = ptx::mapa(ptx::smem_addr(&cb->mb_x[par]), (uint32_t)lane);
-      ptx::st_async_f64x2(dst, a, b, bar);
-    }
-  }
-  ptx::mbar_wait_cluster(ptx::smem_addr(&cb->mb_x[par]), ph);
-  if (threadIdx.x == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[par]), C * 16u);  // arm round+2
-  double2 c = (lane < (int)C) ? cb->xch[par][lane] : make_double2(0.0, 0.0);
-  a = c.x;
-  b = c.y;
-#pragma unroll
-  for (int off = 8; off > 0; off >>= 1) {
-    a += __shfl_down_sync(0xffffffffu, a, off);
-    b += __shfl_down_sync(0xffffffffu, b, off);
-  }
-  a = __shfl_sync(0xffffffffu, a, 0);
-  b = __shfl_sync(0xffffffffu, b, 0);
-  ++round;
-  return make_double2(a, b);
 }
 
 __device__ __forceinline__ bool cand_better(double v, long long i, double bv, long long bi) {
   return (v > bv) || (v == bv && i < bi);
+}
+
+// xor-butterfly over the low `width` lanes' groups (width a power of two <= 32):
+// every lane ends with the combination of its aligned width-group, and because
+// IEEE addition / the argmax rule are commutative, all lanes of a group hold
+// bit-identical values.
+template <int WIDTH>
+__device__ __forceinline__ void bfly_sum2(double& a, double& b) {
+#pragma unroll
+  for (int m = WIDTH / 2; m > 0; m >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, m);
+    b += __shfl_xor_sync(0xffffffffu, b, m);
+  }
+}
+
+template <int WIDTH>
+__device__ __forceinline__ void bfly_argmax(double& best, long long& besti) {
+#pragma unroll
+  for (int m = WIDTH / 2; m > 0; m >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, m);
+    const long long oi = __shfl_xor_sync(0xffffffffu, besti, m);
+    if (cand_better(ov, oi, best, besti)) {
+      best = ov;
+      besti = oi;
+    }
+  }
+}
+
+__device__ __forceinline__ void butterfly_argmax(double& best, long long& besti) { bfly_argmax<32>(best, besti); }
+
+// ---------------------------------------------------------------------------
+// Cluster-wide reduction over one row group: sums of (a, b) and, when ARGMAX,
+// the lexicographic (value desc, index asc) maximum of (best, besti).  All NTG
+// threads of group g must call it; every thread returns the cluster result,
+// bit-identical in every CTA.
+//   warp butterfly -> per-warp partial in smem -> named barrier -> warp 0
+//   combines the NW partials and pushes one 32-byte record into slot [rank] of
+//   every CTA (st.async, complete_tx on the destination's mbarrier) -> every
+//   warp combines the C records in the same fixed butterfly order.
+template <int NTG, bool ARGMAX>
+__device__ __forceinline__ double2 cluster_reduce(double a, double b, double& best, long long& besti, ControlBlock* cb,
+                                                  uint32_t& round, uint32_t rank, uint32_t C, int g, int gtid,
+                                                  long long* tr = nullptr) {
+  constexpr int NW = NTG / 32;
+  const int lane = gtid & 31, warp = gtid >> 5;
+  bfly_sum2<32>(a, b);
+  if (ARGMAX) bfly_argmax<32>(best, besti);
+  if (lane == 0) {
+    cb->wred[warp] = make_double2(a, b);
+    if (ARGMAX) cb->wcand[warp] = make_double2(best, __longlong_as_double(besti));
+  }
+  group_sync<NTG>(g);
+  const uint32_t par = round & 1u, ph = (round >> 1) & 1u;
+  if (warp == 0) {
+    const double2 w = cb->wred[lane & (NW - 1)];
+    double ca = w.x, cbv = w.y;
+    bfly_sum2<NW>(ca, cbv);
+    double cv = -HUGE_VAL;
+    long long ci = 0x7fffffffffffffffLL;
+    if (ARGMAX) {
+      const double2 wc = cb->wcand[lane & (NW - 1)];
+      cv = wc.x;
+      ci = __double_as_longlong(wc.y);
+      bfly_argmax<NW>(cv, ci);
+    }
+    if (lane < (int)C) {
+      const uint32_t bar = ptx::mapa(ptx::smem_addr(&cb->mb_x[par]), (uint32_t)lane);
+      ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->xch[par][rank].ab), (uint32_t)lane), ca, cbv, bar);
+      ptx::st_async_b64x2(ptx::mapa(ptx::smem_addr(&cb->xch[par][rank].cand), (uint32_t)lane),
+                          (uint64_t)__double_as_longlong(cv), (uint64_t)ci, bar);
+    }
+  }
+  PAM_TRACE(tr, 24);
+  ptx::mbar_wait_cta(ptx::smem_addr(&cb->mb_x[par]), ph);
+  PAM_TRACE(tr, 25);
+  if (gtid == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[par]), C * 32u);  // arm round+2
+  const int src = lane & 15;
+  const bool have = src < (int)C;
+  const XchRecord rec = cb->xch[par][have ? src : 0];
+  a = have ? rec.ab.x : 0.0;
+  b = have ? rec.ab.y : 0.0;
+  bfly_sum2<16>(a, b);
+  if (ARGMAX) {
+    best = have ? rec.cand.x : -HUGE_VAL;
+    besti = have ? __double_as_longlong(rec.cand.y) : 0x7fffffffffffffffLL;
+    bfly_argmax<16>(best, besti);
+  }
+  PAM_TRACE(tr, 26);
+  ++round;
+  return make_double2(a, b);
+}
+
+template <int NTG>
+__device__ __forceinline__ double2 cluster_sum2(double a, double b, ControlBlock* cb, uint32_t& round, uint32_t rank,
+                                                uint32_t C, int g, int gtid, long long* tr = nullptr) {
+  double bv = 0.0;
+  long long bi = 0;
+  return cluster_reduce<NTG, false>(a, b, bv, bi, cb, round, rank, C, g, gtid, tr);
 }
 
 // ---------------------------------------------------------------------------
@@ -159,74 +248,92 @@ __device__ __forceinline__ Elem cutmax_update(Elem v, Elem k, Elem b, Elem kn, i
   }
 }
 
-// Per-iteration scalars from the cluster sums.  Returns false if the shift
-// left more than ~1 digit of cancellation (caller then does an exact pass).
-__device__ __forceinline__ void moments_from_sums(double S, double Q, double nd, double& dm, double& s2) {
-  dm = S / nd;
-  s2 = Q / nd - dm * dm;
+__device__ __forceinline__ void moments_from_sums(double S, double Q, double inv_n, double& dm, double& s2) {
+  dm = S * inv_n;
+  s2 = fma(-dm, dm, Q * inv_n);
 }
 
 // ---------------------------------------------------------------------------
-// CutMax on a register-resident row slice.
+// CutMax on a register-resident row slice (one row group).
 //
-// On entry v[] holds the CTA's slice: `len` real elements followed by phantom
-// elements (slots beyond the slice) that the caller filled with K0.  Phantoms
-// keep every pass free of per-element predicates: all phantoms of the row
-// carry one common value w_t (a copy of element 0's trajectory in spirit — they
-// start at K0 and get the same updates), tracked here as a scalar, and their
-// total contribution m*w (m = number of phantoms in the cluster) is subtracted
-// from the cluster sums.
+// On entry v[] holds the group's slice: `len` real elements followed by
+// phantom elements (slots beyond the slice) that the caller filled with K0.
+// Phantoms keep every pass free of per-element predicates: all phantoms of the
+// row carry one common value w_t (they start at K0 and get the same updates),
+// tracked here as a scalar, and their total contribution m*w (m = number of
+// phantoms in the cluster) is subtracted from the cluster sums.
+//
+// With ARGMAX, the last iteration's pass also tracks the argmax of Y^(T+1)
+// (pin A7: equals argmax Z for the positive normaliser) and the last exchange
+// carries it, so no separate gather is needed.  When the caller filled the
+// phantoms with x[0] and K0 = x[0], phantoms are exact copies of element 0 and
+// can never beat it (equal value, larger index), so no predicate is needed.
 //
 // On exit v holds Y^(T+1) (shift 0) and rnorm the normaliser inv(sum Y) (1
 // when PAM_F_NO_NORMALIZE).  Returns the row status, identical in every CTA.
-template <typename Elem, int NT, int E, int P>
+template <typename Elem, int NTG, int E, int P, bool ARGMAX>
 __device__ __forceinline__ int cutmax_core(Elem (&v)[E], const double K0, const double mphantom,
-                                           const RowParams& rp, const double nd, ControlBlock* cb,
-                                           uint32_t& xround, const uint32_t rank, const uint32_t C,
-                                           double* stats_row, double& rnorm) {
+                                           const RowParams& rp, const double inv_n, ControlBlock* cb,
+                                           uint32_t& xround, const uint32_t rank, const uint32_t C, const int g,
+                                           const int gtid, const int64_t gbase, double* stats_row, double& rnorm,
+                                           long long& argmax_out, long long* tr = nullptr) {
+  using Tr = ElemTraits<Elem>;
+  constexpr int VEC = Tr::VEC;
   constexpr double kGuard = sizeof(Elem) == 8 ? 16.0 : 2.0;  // cancellation guard (see header)
   const int T = rp.T;
   const bool normalize = !(rp.flags & PAM_F_NO_NORMALIZE);
   int st = PAM_OK;
   rnorm = 1.0;
+  argmax_out = -1;
 
   // exact second pass about dm when the shifted one-pass moments cancelled
   auto guard = [&](double S, double Q, double w, double& dm, double& s2) {
-    moments_from_sums(S, Q, nd, dm, s2);
-    if (st == PAM_OK && isfinite(Q) && Q / nd > kGuard * s2) {
+    moments_from_sums(S, Q, inv_n, dm, s2);
+    if (st == PAM_OK && isfinite(Q) && Q * inv_n > kGuard * s2) {
       const Elem dme = (Elem)dm;
-      Elem q2 = 0;
+      Elem q2a = 0, q2b = 0;
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const Elem d = v[i] - dme;
-        q2 = fma_e(d, d, q2);
+      for (int i = 0; i < E; i += 2) {
+        const Elem d0 = v[i] - dme, d1 = v[i + 1] - dme;
+        q2a = fma_e(d0, d0, q2a);
+        q2b = fma_e(d1, d1, q2b);
       }
-      const double2 r2 = cluster_sum2<NT>((double)q2, 0.0, cb, xround, rank, C);
+      const double2 r2 = cluster_sum2<NTG>((double)q2a + (double)q2b, 0.0, cb, xround, rank, C, g, gtid);
       const Elem dw = (Elem)w - dme;
-      s2 = (r2.x - mphantom * (double)dw * (double)dw) / nd;
+      s2 = (r2.x - mphantom * (double)dw * (double)dw) * inv_n;
     }
   };
+
+  // per-iteration constants, loaded ahead of the exchange they follow
+  double c_inv = rp.inv_c[0], knext = rp.kshift[1];
+  int pcur = rp.p[0];
 
   // ---- input pass: shift by K0 (phantoms hold K0 -> contribute exactly 0) ---
   double dm, s2;
   {
     const Elem k0 = (Elem)K0;
-    Elem s = 0, q = 0;
+    Elem sa = 0, sb = 0, qa = 0, qb = 0;
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const Elem d = v[i] - k0;
-      v[i] = d;
-      s += d;
-      q = fma_e(d, d, q);
+    for (int i = 0; i < E; i += 2) {
+      const Elem d0 = v[i] - k0, d1 = v[i + 1] - k0;
+      v[i] = d0;
+      v[i + 1] = d1;
+      sa += d0;
+      sb += d1;
+      qa = fma_e(d0, d0, qa);
+      qb = fma_e(d1, d1, qb);
     }
-    const double2 r = cluster_sum2<NT>((double)s, (double)q, cb, xround, rank, C);
+    PAM_TRACE(tr, 3);
+    const double2 r =
+        cluster_sum2<NTG>((double)sa + (double)sb, (double)qa + (double)qb, cb, xround, rank, C, g, gtid, tr);
+    PAM_TRACE(tr, 4);
     if (!isfinite(r.x) || !isfinite(r.y)) st = PAM_ERR_NON_FINITE;
     guard(r.x, r.y, 0.0, dm, s2);
   }
   double kcur = K0;
   Elem w = 0;  // phantom value (shifted representation)
 
-  // ---- T iterations; the last one (no variance needed) is peeled ------------
+  // ---- T iterations; the last one (no variance; argmax) is peeled -----------
   double total = 0.0;
   for (int t = 0; t < T; ++t) {
     const double mu = kcur + dm;
@@ -243,49 +350,75 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], const double K0, const 
         const int rs = invsqrt_rescaled(s2, ac.iterations, ac.rescale, ac.scale_log2, ac.lo, ac.hi, &inv_sigma);
         if (rs) st = rs;
       } else {
-        inv_sigma = 1.0 / sqrt(s2);
+        inv_sigma = rsqrt(s2);  // ~1 ulp; identical in every CTA of the cluster
       }
     }
-    const double kd = (st == PAM_OK) ? inv_sigma * rp.inv_c[t] : 0.0;
+    const double kd = (st == PAM_OK) ? inv_sigma * c_inv : 0.0;
     const double bd = fma(-dm, kd, 1.0);
-    const double knext = rp.kshift[t + 1];
     const Elem ke = (Elem)kd, be = (Elem)bd, kn = (Elem)(-knext);
-    const int p = rp.p[t];
+    const int p = pcur;
+    if (t == 0) PAM_TRACE(tr, 27);
     w = cutmax_update<Elem, P>(w, ke, be, kn, p);
+    const double kthis = knext;
     if (t + 1 < T) {
-      Elem s = 0, q = 0;
+      Elem sa = 0, sb = 0, qa = 0, qb = 0;
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const Elem d = cutmax_update<Elem, P>(v[i], ke, be, kn, p);
-        v[i] = d;
-        s += d;
-        q = fma_e(d, d, q);
+      for (int i = 0; i < E; i += 2) {
+        const Elem d0 = cutmax_update<Elem, P>(v[i], ke, be, kn, p);
+        const Elem d1 = cutmax_update<Elem, P>(v[i + 1], ke, be, kn, p);
+        v[i] = d0;
+        v[i + 1] = d1;
+        sa += d0;
+        sb += d1;
+        qa = fma_e(d0, d0, qa);
+        qb = fma_e(d1, d1, qb);
       }
-      const double2 r = cluster_sum2<NT>((double)s, (double)q, cb, xround, rank, C);
+      c_inv = rp.inv_c[t + 1];  // prefetch next iteration's constants
+      knext = rp.kshift[t + 2];
+      pcur = rp.p[t + 1];
+      PAM_TRACE(tr, 5 + 2 * t);
+      const double2 r =
+          cluster_sum2<NTG>((double)sa + (double)sb, (double)qa + (double)qb, cb, xround, rank, C, g, gtid);
+      PAM_TRACE(tr, 6 + 2 * t);
       const double wd = (double)w;
       guard(r.x - mphantom * wd, r.y - mphantom * wd * wd, wd, dm, s2);
-      kcur = knext;
+      kcur = kthis;
     } else {
-      Elem s = 0;
+      Elem sa = 0, sb = 0;
+      double best = -HUGE_VAL;
+      long long besti = 0x7fffffffffffffffLL;
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const Elem d = cutmax_update<Elem, P>(v[i], ke, be, kn, p);
-        v[i] = d;
-        s += d;
+      for (int i = 0; i < E; i += 2) {
+        const Elem d0 = cutmax_update<Elem, P>(v[i], ke, be, kn, p);
+        const Elem d1 = cutmax_update<Elem, P>(v[i + 1], ke, be, kn, p);
+        v[i] = d0;
+        v[i + 1] = d1;
+        sa += d0;
+        sb += d1;
+        if (ARGMAX) {
+          // element index: k-th vector of this thread, lane j (increasing with i)
+          const long long idx0 = gbase + (long long)(((i / VEC) * NTG + gtid) * VEC + (i % VEC));
+          if ((double)d0 > best) { best = (double)d0; besti = idx0; }
+          if ((double)d1 > best) { best = (double)d1; besti = idx0 + 1; }
+        }
       }
-      const double2 r = cluster_sum2<NT>((double)s, 0.0, cb, xround, rank, C);
+      PAM_TRACE(tr, 5 + 2 * t);
+      const double2 r = cluster_reduce<NTG, ARGMAX>((double)sa + (double)sb, 0.0, best, besti, cb, xround, rank, C,
+                                                    g, gtid);
+      PAM_TRACE(tr, 6 + 2 * t);
       total = r.x - mphantom * (double)w;  // kshift[T] == 0: v holds Y^(T+1) itself
+      argmax_out = besti;
     }
   }
 
   if (st == PAM_OK && !isfinite(total)) st = PAM_ERR_RANGE;
   if (st == PAM_OK && normalize) {
-    if (rp.inv_mode == PAM_MODE_POLY) {
+    if (!(total > 0.0)) {
+      st = PAM_ERR_RANGE;  // Z must be a distribution (pin A7)
+    } else if (rp.inv_mode == PAM_MODE_POLY) {
       const pam_approx_config& ac = rp.inv;
       const int rs = inv_rescaled(total, ac.iterations, ac.rescale, ac.scale_log2, ac.lo, ac.hi, &rnorm);
       if (rs) st = rs;
-    } else if (total == 0.0) {
-      st = PAM_ERR_RANGE;
     } else {
       rnorm = 1.0 / total;
     }
@@ -293,23 +426,31 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], const double K0, const 
   return st;
 }
 
+// Resident CTAs per SM the register budget should allow (launch-bounds hint).
+template <typename Elem, int NT, int E>
+constexpr int min_blocks_for() {
+  constexpr int regs = E * (int)sizeof(Elem) / 4 + 48;
+  constexpr int b = 65536 / (NT * regs);
+  return b < 1 ? 1 : (b > 8 ? 8 : b);
+}
+
 // ---------------------------------------------------------------------------
-template <typename Elem, int NT, int E, int P, bool TMA>
-__global__ void __launch_bounds__(NT, 1) cutmax_rows_kernel(const CutmaxArgs a) {
+template <typename Elem, int NTG, int G, int E, int P>
+__global__ void __launch_bounds__(NTG* G, (min_blocks_for<Elem, NTG * G, E>())) cutmax_rows_kernel(const CutmaxArgs a) {
   using Tr = ElemTraits<Elem>;
   using V = typename Tr::V;
   constexpr int VEC = Tr::VEC;
   constexpr int NV = E / VEC;
-  constexpr int NW = NT / 32;
-  static_assert(E % VEC == 0, "E must be a multiple of the vector width");
-  static_assert(NT % 32 == 0 && NW <= 32, "bad block size");
+  constexpr int NW = NTG / 32;
+  static_assert(E % VEC == 0 && E % 2 == 0, "E must be a multiple of the vector width");
+  static_assert(NTG % 32 == 0 && NW <= 16 && (NW & (NW - 1)) == 0, "bad group size");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Elem* buf = reinterpret_cast<Elem*>(smem_raw);
-  ControlBlock* cb = reinterpret_cast<ControlBlock*>(smem_raw + a.ctrl_offset);
+  const int g = (G == 1) ? 0 : (int)(threadIdx.x / NTG);
+  const int gtid = (G == 1) ? (int)threadIdx.x : (int)(threadIdx.x % NTG);
+  Elem* buf = reinterpret_cast<Elem*>(smem_raw + g * a.buf_bytes);
+  ControlBlock* cb = reinterpret_cast<ControlBlock*>(smem_raw + a.ctrl_offset) + g;
 
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
   const uint32_t rank = ptx::cluster_ctarank();
   const uint32_t C = ptx::cluster_nctarank();
   const int64_t cid = ptx::cluster_id_x();
@@ -318,8 +459,8 @@ __global__ void __launch_bounds__(NT, 1) cutmax_rows_kernel(const CutmaxArgs a) 
   const int64_t base = (int64_t)rank * a.L;
   const int64_t rem = n - base;
   const int len = rem <= 0 ? 0 : (rem < a.L ? (int)rem : a.L);
-  const double nd = (double)n;
-  const double mphantom = (double)((int64_t)C * NT * E - n);  // phantom slots in the cluster
+  const bool TMA = a.tma != 0;
+  const double mphantom = (double)((int64_t)C * NTG * E - n);  // phantom slots in the cluster
   const RowParams& rp = a.rp;
   const int T = rp.T;
   const Elem* __restrict__ X = reinterpret_cast<const Elem*>(a.x);
@@ -330,18 +471,16 @@ __global__ void __launch_bounds__(NT, 1) cutmax_rows_kernel(const CutmaxArgs a) 
   uint64_t policy = 0;
   if (TMA) policy = ptx::policy_evict_first();
 
-  if (tid == 0) {
+  if (gtid == 0) {
     ptx::mbar_init(bar_load, 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[0]), 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[1]), 1);
-    ptx::mbar_init(ptx::smem_addr(&cb->mb_a), 1);
     ptx::fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 16u);
-    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 16u);
-    if (rank == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_a), C * 16u);
+  if (gtid == 0) {
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 32u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 32u);
   }
   ptx::cluster_sync();
 
@@ -356,24 +495,39 @@ __global__ void __launch_bounds__(NT, 1) cutmax_rows_kernel(const CutmaxArgs a) 
     }
   };
 
-  uint32_t xround = 0, load_par = 0, a_par = 0;
-  if (TMA && tid == 0 && cid < a.B) issue_load(cid);
+  const int64_t row0 = cid * G + g, rstride = ncl * G;
+  uint32_t xround = 0, load_par = 0;
+  if (TMA && gtid == 0 && row0 < a.B) issue_load(row0);
+  // De-phase the row streams: identical clusters started together stay in
+  // lockstep and hit their HBM store bursts and exchanges at the same time.
+  // Row stream s = g*ncl + cid starts s/(G*ncl) of a row period late.
+  if (a.stagger > 0) {
+    const long long wait = a.stagger * (long long)(g * ncl + cid) / (long long)(G * ncl);
+    const long long t0 = clock64();
+    while (clock64() - t0 < wait) __nanosleep(256);
+  }
 
   Elem v[E];
 
-  for (int64_t row = cid; row < a.B; row += ncl) {
+  for (int64_t row = row0; row < a.B; row += rstride) {
+    const int64_t lrow = (row - row0) / rstride;
+    long long* tr = (a.trace && g == 0 && lrow < kTraceRows)
+                        ? a.trace + ((int64_t)blockIdx.x * kTraceRows + lrow) * kTraceEvents
+                        : nullptr;
+    PAM_TRACE(tr, 0);
     const Elem* xrow = X + row * a.ldx;
-    const Elem k0e = __ldg(xrow);           // shift for the input pass (same in every CTA)
+    const Elem k0e = __ldg(xrow);  // shift for the input pass (same in every CTA)
     const double K0 = (double)k0e;
-    __syncthreads();                          // previous row fully retired (wred / cand reuse)
+    group_sync<NTG>(g);  // previous row fully retired (wred / cand reuse)
 
     // ---- load the slice into registers --------------------------------------
     if (TMA) {
       ptx::mbar_wait_cta(bar_load, load_par);
       load_par ^= 1u;
+      PAM_TRACE(tr, 1);
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
-        const int li0 = (k * NT + tid) * VEC;
+        const int li0 = (k * NTG + gtid) * VEC;
         if (li0 + VEC <= len) {
           const V t = *reinterpret_cast<const V*>(buf + li0);
           *reinterpret_cast<V*>(&v[k * VEC]) = t;
@@ -382,41 +536,41 @@ __global__ void __launch_bounds__(NT, 1) cutmax_rows_kernel(const CutmaxArgs a) 
           for (int j = 0; j < VEC; ++j) v[k * VEC + j] = (li0 + j < len) ? buf[li0 + j] : k0e;  // phantoms = K0
         }
       }
-      __syncthreads();  // landing buffer free: prefetch the next row of this cluster
-      if (tid == 0 && row + ncl < a.B) issue_load(row + ncl);
+      group_sync<NTG>(g);  // landing buffer free: prefetch the next row of this group
+      if (gtid == 0 && row + rstride < a.B) issue_load(row + rstride);
+      PAM_TRACE(tr, 2);
     } else {
       const Elem* src = xrow + base;
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
-        const int li0 = (k * NT + tid) * VEC;
+        const int li0 = (k * NTG + gtid) * VEC;
 #pragma unroll
         for (int j = 0; j < VEC; ++j) v[k * VEC + j] = (li0 + j < len) ? __ldcs(src + li0 + j) : k0e;
       }
     }
 
-    // ---- input statistics + T CutMax iterations + normaliser -------------------
+    // ---- input statistics + T CutMax iterations + normaliser + argmax ------------
     double rnorm = 1.0;
-    int st = cutmax_core<Elem, NT, E, P>(v, K0, mphantom, rp, nd, cb, xround, rank, C,
-                                         (rank == 0 && tid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr,
-                                         rnorm);
+    long long amax = -1;
+    const int st = cutmax_core<Elem, NTG, E, P, true>(
+        v, K0, mphantom, rp, a.inv_n, cb, xround, rank, C, g, gtid, base,
+        (rank == 0 && gtid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr, rnorm, amax, tr);
+    PAM_TRACE(tr, 20);
+    if (rank == 0 && gtid == 0) {
+      if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)amax : -1;
+      if (a.status) a.status[row] = st;
+    }
 
-    // ---- normalisation, argmax, store ----------------------------------------
+    // ---- Z = Y * inv(sum Y), streamed out with 128-bit evict-first stores -------
     const Elem re = (Elem)rnorm;
-    double best = -HUGE_VAL;
-    long long besti = 0x7fffffffffffffffLL;
     Elem* zrow = Z + row * a.ldz + base;
+    if (!(a.debug_flags & 1))
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      const int li0 = (k * NT + tid) * VEC;
+      const int li0 = (k * NTG + gtid) * VEC;
       Elem o[VEC];
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        o[j] = v[k * VEC + j] * re;
-        if (li0 + j < len && (double)o[j] > best) {
-          best = (double)o[j];
-          besti = base + li0 + j;
-        }
-      }
+      for (int j = 0; j < VEC; ++j) o[j] = v[k * VEC + j] * re;
       if (TMA && li0 + VEC <= len) {
         __stcs(reinterpret_cast<V*>(zrow + li0), *reinterpret_cast<V*>(o));
       } else {
@@ -425,50 +579,7 @@ __global__ void __launch_bounds__(NT, 1) cutmax_rows_kernel(const CutmaxArgs a) 
           if (li0 + j < len) __stcs(zrow + li0 + j, o[j]);
       }
     }
-    // argmax: warp tree -> CTA -> gather to rank 0 (lowest index wins ties)
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double ov = __shfl_down_sync(0xffffffffu, best, off);
-      const long long oi = __shfl_down_sync(0xffffffffu, besti, off);
-      if (cand_better(ov, oi, best, besti)) { best = ov; besti = oi; }
-    }
-    if (lane == 0) cb->wred[warp] = make_double2(best, __longlong_as_double(besti));
-    __syncthreads();
-    if (warp == 0) {
-      double2 w = (lane < NW) ? cb->wred[lane] : make_double2(-HUGE_VAL, __longlong_as_double(0x7fffffffffffffffLL));
-      best = w.x;
-      besti = __double_as_longlong(w.y);
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_down_sync(0xffffffffu, best, off);
-        const long long oi = __shfl_down_sync(0xffffffffu, besti, off);
-        if (cand_better(ov, oi, best, besti)) { best = ov; besti = oi; }
-      }
-      if (lane == 0) {
-        const uint32_t dst = ptx::mapa(ptx::smem_addr(&cb->cand[rank]), 0u);
-        const uint32_t bar = ptx::mapa(ptx::smem_addr(&cb->mb_a), 0u);
-        ptx::st_async_b64x2(dst, (uint64_t)__double_as_longlong(best), (uint64_t)besti, bar);
-      }
-      if (rank == 0) {
-        ptx::mbar_wait_cluster(ptx::smem_addr(&cb->mb_a), a_par);
-        a_par ^= 1u;
-        double2 w2 = (lane < (int)C) ? cb->cand[lane]
-                                     : make_double2(-HUGE_VAL, __longlong_as_double(0x7fffffffffffffffLL));
-        best = w2.x;
-        besti = __double_as_longlong(w2.y);
-#pragma unroll
-        for (int off = 8; off > 0; off >>= 1) {
-          const double ov = __shfl_down_sync(0xffffffffu, best, off);
-          const long long oi = __shfl_down_sync(0xffffffffu, besti, off);
-          if (cand_better(ov, oi, best, besti)) { best = ov; besti = oi; }
-        }
-        if (lane == 0) {
-          ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_a), C * 16u);  // arm next row
-          if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)besti : -1;
-          if (a.status) a.status[row] = st;
-        }
-      }
-    }
+    PAM_TRACE(tr, 21);
   }
   ptx::cluster_sync();  // no CTA leaves while a peer may still push into its shared memory
 }

@@ -33,6 +33,7 @@ struct SamplerArgs {
   double p_nucleus;
   uint64_t seed, draw;
   int32_t tma;  // 1: TMA bulk load (16-byte aligned rows), 0: thread copy
+  double inv_n;
   RowParams rp;
 };
 
@@ -57,7 +58,6 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
   const int64_t base = (int64_t)rank * a.L;
   const int64_t rem = n - base;
   const int len = rem <= 0 ? 0 : (rem < a.L ? (int)rem : a.L);
-  const double nd = (double)n;
   const double mphantom = (double)((int64_t)C * NT * E - n);
   const uint32_t bar_load = ptx::smem_addr(&cb->mb_load);
   const uint32_t load_bytes = (uint32_t)len * 8u;
@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
   }
   __syncthreads();
   if (tid == 0) {
-    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 16u);
-    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 16u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 32u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 32u);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_g), C * 32u);
   }
   ptx::cluster_sync();
@@ -134,7 +134,9 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     }
 
     double rnorm = 1.0;
-    int st = cutmax_core<double, NT, E, P>(v, K0, mphantom, a.rp, nd, cb, xround, rank, C, nullptr, rnorm);
+    long long unused_argmax;
+    int st = cutmax_core<double, NT, E, P, false>(v, K0, mphantom, a.rp, a.inv_n, cb, xround, rank, C, 0, tid, base,
+                                                  nullptr, rnorm, unused_argmax);
 
     // token candidate over Z = Y * rnorm (and optional one-hot store)
     double best = -HUGE_VAL, bestx = 0.0;
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
         }
       }
     }
-    const double2 ta = cluster_sum2<NT>(tot, above, cb, xround, rank, C);
+    const double2 ta = cluster_sum2<NT>(tot, above, cb, xround, rank, C, 0, tid);
     if (rank == 0 && tid == 0) {
       if (a.token) a.token[row] = (st == PAM_OK) ? (int32_t)besti : -1;
       if (a.inside) a.inside[row] = (st == PAM_OK && ta.y < a.p_nucleus * ta.x) ? 1 : 0;

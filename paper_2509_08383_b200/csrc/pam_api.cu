@@ -23,6 +23,8 @@ using namespace pam;
 namespace {
 
 std::atomic<int64_t> g_launches{0};
+long long* g_trace = nullptr;  // debug phase-trace buffer (pam_set_trace_buffer)
+int64_t g_trace_entries = 0;
 thread_local char g_last_err[256] = "";
 
 int cuda_fail(cudaError_t e, const char* what) {
@@ -38,34 +40,37 @@ struct Geometry {
   int L = 0;
 };
 
-bool parse_force(int elem_bytes, int* nt, int* e, int* c) {
+bool parse_force(int elem_bytes, int* ntg, int* e, int* c, int* g) {
   const char* s = getenv(elem_bytes == 8 ? "PAM_FORCE_CFG_F64" : "PAM_FORCE_CFG_F32");
   if (!s || !*s) return false;
-  return sscanf(s, "%d,%d,%d", nt, e, c) == 3;
+  *g = 1;
+  return sscanf(s, "%d,%d,%d,%d", ntg, e, c, g) >= 3;
 }
+
+int64_t slice_len(int64_t n, int C, int vec) { return ((n + C - 1) / C + vec - 1) / vec * vec; }
 
 Geometry choose_geometry(int elem_bytes, int64_t B, int64_t n) {
   Geometry g;
   const int vec = 16 / elem_bytes;
-  int fnt, fe, fc;
-  if (parse_force(elem_bytes, &fnt, &fe, &fc)) {
+  int fntg, fe, fc, fg;
+  if (parse_force(elem_bytes, &fntg, &fe, &fc, &fg)) {
     for (int i = 0; i < kNumCutmaxVariants; ++i) {
       const Variant& v = kCutmaxVariants[i];
-      if (v.elem_bytes == elem_bytes && v.nt == fnt && v.e == fe) {
-        const int64_t L = ((n + fc - 1) / fc + vec - 1) / vec * vec;
-        if ((int64_t)v.nt * v.e >= L) { g.var = &v; g.C = fc; g.L = (int)L; return g; }
+      if (v.elem_bytes == elem_bytes && v.ntg == fntg && v.e == fe && v.g == fg) {
+        const int64_t L = slice_len(n, fc, vec);
+        if ((int64_t)v.ntg * v.e >= L) { g.var = &v; g.C = fc; g.L = (int)L; return g; }
       }
     }
   }
   (void)B;
   for (int C = 1; C <= 16; C *= 2) {
-    const int64_t L = ((n + C - 1) / C + vec - 1) / vec * vec;
+    const int64_t L = slice_len(n, C, vec);
     const Variant* best = nullptr;
     for (int i = 0; i < kNumCutmaxVariants; ++i) {
       const Variant& v = kCutmaxVariants[i];
-      if (v.elem_bytes != elem_bytes) continue;
-      if ((int64_t)v.nt * v.e < L) continue;
-      if (!best || (int64_t)v.nt * v.e < (int64_t)best->nt * best->e) best = &v;
+      if (v.elem_bytes != elem_bytes || v.g != 1) continue;
+      if ((int64_t)v.ntg * v.e < L) continue;
+      if (!best || (int64_t)v.ntg * v.e < (int64_t)best->ntg * best->e) best = &v;
     }
     if (best) { g.var = best; g.C = C; g.L = (int)L; return g; }
   }
@@ -183,12 +188,15 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
                    (ld_z % vec == 0) && (n % vec == 0) && getenv("PAM_DISABLE_TMA") == nullptr;
   bool p3 = true;
   for (int t = 0; t < prm->T; ++t) p3 = p3 && (prm->p[t] == 3);
-  const void* fn = g.var->fn[p3 ? 1 : 0][tma ? 1 : 0];
+  const void* fn = g.var->fn[p3 ? 1 : 0];
+  const int G = g.var->g;
   const int buf_bytes = tma ? ((g.L * (int)sizeof(Elem) + 127) / 128) * 128 : 0;
-  const int smem = buf_bytes + (int)sizeof(ControlBlock);
-  const int maxcl = max_active_clusters(fn, g.var->nt, g.C, smem);
+  const int smem = G * (buf_bytes + (int)sizeof(ControlBlock));
+  const int nt = g.var->ntg * G;
+  const int maxcl = max_active_clusters(fn, nt, g.C, smem);
   if (maxcl <= 0) return cuda_fail(cudaErrorInvalidConfiguration, "no cluster fits (occupancy 0)");
-  const int clusters = (int)(B < maxcl ? B : maxcl);
+  const int64_t want = (B + G - 1) / G;
+  const int clusters = (int)(want < maxcl ? want : maxcl);
   CutmaxArgs ka;
   memset(&ka, 0, sizeof ka);
   ka.x = d_x;
@@ -201,9 +209,19 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   ka.B = B;
   ka.n = n;
   ka.L = g.L;
-  ka.ctrl_offset = buf_bytes;
+  ka.buf_bytes = buf_bytes;
+  ka.ctrl_offset = G * buf_bytes;
+  ka.tma = tma ? 1 : 0;
+  ka.inv_n = 1.0 / (double)n;
+  {
+    const char* sg = getenv("PAM_STAGGER");
+    ka.stagger = sg ? atoll(sg) : 0;
+    const char* df = getenv("PAM_DEBUG_FLAGS");
+    ka.debug_flags = df ? atoi(df) : 0;
+  }
+  if (g_trace && (int64_t)clusters * g.C * kTraceRows * kTraceEvents <= g_trace_entries) ka.trace = g_trace;
   fill_row_params(prm, &ka.rp);
-  return launch_cluster_kernel(fn, g.var->nt, g.C, clusters, smem, stream, &ka);
+  return launch_cluster_kernel(fn, nt, g.C, clusters, smem, stream, &ka);
 }
 
 int sampler_batch_impl(const double* d_x, int64_t ld_x, int64_t B, int64_t n, const pam_sampler_cfg* cfg,
@@ -259,6 +277,7 @@ int sampler_batch_impl(const double* d_x, int64_t ld_x, int64_t B, int64_t n, co
   sa.p_nucleus = cfg->p;
   sa.seed = cfg->seed;
   sa.draw = cfg->draw;
+  sa.inv_n = 1.0 / (double)n;
   sa.tma = ((uintptr_t)d_x % 16 == 0) && (ld_x % 2 == 0) && (n % 2 == 0) && getenv("PAM_DISABLE_TMA") == nullptr;
   fill_row_params(prm, &sa.rp);
   return launch_cluster_kernel(fn, var->nt, C, clusters, smem, stream, &sa);
@@ -487,22 +506,30 @@ int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_par
   bool p3 = true;
   if (prm)
     for (int t = 0; t < prm->T; ++t) p3 = p3 && (prm->p[t] == 3);
-  const void* fn = g.var->fn[p3 ? 1 : 0][1];
+  const void* fn = g.var->fn[p3 ? 1 : 0];
+  const int G = g.var->g;
   const int buf_bytes = ((g.L * dtype_bytes + 127) / 128) * 128;
-  const int smem = buf_bytes + (int)sizeof(ControlBlock);
-  info->threads = g.var->nt;
+  const int smem = G * (buf_bytes + (int)sizeof(ControlBlock));
+  info->threads = g.var->ntg * G;
   info->elems_per_thread = g.var->e;
   info->cluster = g.C;
   info->smem_bytes = smem;
   info->tma = 1;
-  const int maxcl = max_active_clusters(fn, g.var->nt, g.C, smem);
-  info->clusters = (int)(B < maxcl ? B : maxcl);
+  const int maxcl = max_active_clusters(fn, info->threads, g.C, smem);
+  const int64_t want = (B + G - 1) / G;
+  info->clusters = (int)(want < maxcl ? want : maxcl);
   info->ctas = info->clusters * g.C;
+  info->groups = G;
   info->kernel_id = (int)(g.var - kCutmaxVariants);
   return PAM_OK;
 }
 
 int64_t pam_kernel_launch_count(void) { return g_launches.load(); }
+
+void pam_set_trace_buffer(long long* d_buf, int64_t entries) {
+  g_trace = d_buf;
+  g_trace_entries = d_buf ? entries : 0;
+}
 
 const char* pam_last_cuda_error(void) { return g_last_err; }
 

@@ -6,8 +6,8 @@
 namespace pam {
 
 struct Variant {
-  int elem_bytes, nt, e;
-  const void* fn[2][2];  // [P==3][TMA]
+  int elem_bytes, ntg, g, e;  // threads per row group, row groups per CTA, elements per thread
+  const void* fn[2];          // [P==3]
 };
 
 struct SamplerVariant {
