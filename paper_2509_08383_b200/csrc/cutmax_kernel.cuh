@@ -124,6 +124,37 @@ __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(NTG) : "memory");
 }
 
+// Strict alternation of the fp64 element passes of the G=2 row groups of a CTA.
+// A group holds the token while it streams its slice through the fp64 pipe and
+// hands it over before waiting in its cluster exchange, so one group's
+// exchange latency overlaps the other group's pass.  Named barrier 3+g carries
+// the token to group g (the giver arrives, the taker syncs: 2*NTG threads).
+// Group 0 starts with the token; every group takes and gives exactly
+// K*(T+1) times except that group 0 skips its first take and group 1 its last
+// give, which keeps the barrier arrivals balanced.  G=1: no-ops.
+template <int NTG, int G>
+struct PassToken {
+  int g;
+  int64_t left;  // gives still to perform
+  bool skip_take;
+  __device__ __forceinline__ PassToken(int g_, int64_t total) : g(g_), left(total - (g_ == 1 ? 1 : 0)), skip_take(g_ == 0) {}
+  __device__ __forceinline__ void take() {
+    if (G == 2) {
+      if (skip_take) {
+        skip_take = false;
+      } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(3 + g), "r"(2 * NTG) : "memory");
+      }
+    }
+  }
+  __device__ __forceinline__ void give() {
+    if (G == 2 && left > 0) {
+      --left;
+      asm volatile("bar.arrive %0, %1;" ::"r"(3 + (g ^ 1)), "r"(2 * NTG) : "memory");
+    }
+  }
+};
+
 __device__ __forceinline__ void butterfly_sum2(double& a, double& b) {
 #pragma unroll
   for (int m = 16; m > 0; m >>= 1) {
@@ -271,17 +302,26 @@ __device__ __forceinline__ void moments_from_sums(double S, double Q, double inv
 //
 // On exit v holds Y^(T+1) (shift 0) and rnorm the normaliser inv(sum Y) (1
 // when PAM_F_NO_NORMALIZE).  Returns the row status, identical in every CTA.
-template <typename Elem, int NTG, int E, int P, bool ARGMAX>
-__device__ __forceinline__ int cutmax_core(Elem (&v)[E], const double K0, const double mphantom,
+struct NoOp {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <typename Elem, int NTG, int G, int E, int P, bool ARGMAX, typename AfterFirstXchg = NoOp>
+__device__ __forceinline__ int cutmax_core(Elem (&v)[E], PassToken<NTG, G>& tok, const double K0, const double mphantom,
                                            const RowParams& rp, const double inv_n, ControlBlock* cb,
                                            uint32_t& xround, const uint32_t rank, const uint32_t C, const int g,
                                            const int gtid, const int64_t gbase, double* stats_row, double& rnorm,
-                                           long long& argmax_out, long long* tr = nullptr) {
+                                           long long& argmax_out, long long* tr = nullptr,
+                                           const AfterFirstXchg& after_first_xchg = AfterFirstXchg()) {
   using Tr = ElemTraits<Elem>;
   constexpr int VEC = Tr::VEC;
   constexpr double kGuard = sizeof(Elem) == 8 ? 16.0 : 2.0;  // cancellation guard (see header)
+  // kernel parameters the per-iteration scalar chain needs, held in registers
+  // (the exchanges' memory clobbers would otherwise re-load them every round)
   const int T = rp.T;
   const bool normalize = !(rp.flags & PAM_F_NO_NORMALIZE);
+  const bool poly_invsqrt = rp.invsqrt_mode == PAM_MODE_POLY;
+  const double eps_var = rp.eps_var;
   int st = PAM_OK;
   rnorm = 1.0;
   argmax_out = -1;
@@ -324,11 +364,14 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], const double K0, const 
       qb = fma_e(d1, d1, qb);
     }
     PAM_TRACE(tr, 3);
+    tok.give();
     const double2 r =
         cluster_sum2<NTG>((double)sa + (double)sb, (double)qa + (double)qb, cb, xround, rank, C, g, gtid, tr);
     PAM_TRACE(tr, 4);
+    if (T == 1) after_first_xchg();
     if (!isfinite(r.x) || !isfinite(r.y)) st = PAM_ERR_NON_FINITE;
     guard(r.x, r.y, 0.0, dm, s2);
+    PAM_TRACE(tr, 28);
   }
   double kcur = K0;
   Elem w = 0;  // phantom value (shifted representation)
@@ -337,22 +380,26 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], const double K0, const 
   double total = 0.0;
   for (int t = 0; t < T; ++t) {
     const double mu = kcur + dm;
-    if (st == PAM_OK && (!isfinite(mu) || !isfinite(s2))) st = PAM_ERR_RANGE;
-    if (st == PAM_OK && s2 < rp.eps_var) st = PAM_ERR_DEGENERATE_INPUT;
+    // status: first failure wins (branch-free on the common path)
+    const bool bad_range = !isfinite(mu) || !isfinite(s2);
+    st = (st != PAM_OK) ? st : (bad_range ? PAM_ERR_RANGE : (s2 < eps_var ? PAM_ERR_DEGENERATE_INPUT : PAM_OK));
     if (stats_row) {
       stats_row[t * 2 + 0] = mu;
       stats_row[t * 2 + 1] = s2;
     }
-    double inv_sigma = 0.0;
-    if (st == PAM_OK) {
-      if (rp.invsqrt_mode == PAM_MODE_POLY) {
-        const pam_approx_config& ac = rp.invsqrt[t];
+    if (t == 0) PAM_TRACE(tr, 29);
+    double inv_sigma;
+    if (!poly_invsqrt) {
+      inv_sigma = rsqrt(s2);  // ~1 ulp; identical in every CTA of the cluster
+    } else {
+      const pam_approx_config& ac = rp.invsqrt[t];
+      inv_sigma = 0.0;
+      if (st == PAM_OK) {
         const int rs = invsqrt_rescaled(s2, ac.iterations, ac.rescale, ac.scale_log2, ac.lo, ac.hi, &inv_sigma);
         if (rs) st = rs;
-      } else {
-        inv_sigma = rsqrt(s2);  // ~1 ulp; identical in every CTA of the cluster
       }
     }
+    if (t == 0) PAM_TRACE(tr, 30);
     const double kd = (st == PAM_OK) ? inv_sigma * c_inv : 0.0;
     const double bd = fma(-dm, kd, 1.0);
     const Elem ke = (Elem)kd, be = (Elem)bd, kn = (Elem)(-knext);
@@ -360,6 +407,7 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], const double K0, const 
     if (t == 0) PAM_TRACE(tr, 27);
     w = cutmax_update<Elem, P>(w, ke, be, kn, p);
     const double kthis = knext;
+    tok.take();
     if (t + 1 < T) {
       Elem sa = 0, sb = 0, qa = 0, qb = 0;
 #pragma unroll
@@ -377,16 +425,21 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], const double K0, const 
       knext = rp.kshift[t + 2];
       pcur = rp.p[t + 1];
       PAM_TRACE(tr, 5 + 2 * t);
+      tok.give();
       const double2 r =
           cluster_sum2<NTG>((double)sa + (double)sb, (double)qa + (double)qb, cb, xround, rank, C, g, gtid);
       PAM_TRACE(tr, 6 + 2 * t);
+      // deferred work (the next-row prefetch into the landing buffer): the
+      // previous row's Z bulk store drains at the HBM write rate and holds the
+      // buffer for several exchanges, so wait until the third exchange
+      if (t == 1 || (t == 0 && T == 2)) after_first_xchg();
       const double wd = (double)w;
       guard(r.x - mphantom * wd, r.y - mphantom * wd * wd, wd, dm, s2);
       kcur = kthis;
     } else {
       Elem sa = 0, sb = 0;
-      double best = -HUGE_VAL;
-      long long besti = 0x7fffffffffffffffLL;
+      Elem bestv = -INFINITY;
+      int besto = 0;  // register slot of the best element (compile-time immediates)
 #pragma unroll
       for (int i = 0; i < E; i += 2) {
         const Elem d0 = cutmax_update<Elem, P>(v[i], ke, be, kn, p);
@@ -395,14 +448,15 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], const double K0, const 
         v[i + 1] = d1;
         sa += d0;
         sb += d1;
-        if (ARGMAX) {
-          // element index: k-th vector of this thread, lane j (increasing with i)
-          const long long idx0 = gbase + (long long)(((i / VEC) * NTG + gtid) * VEC + (i % VEC));
-          if ((double)d0 > best) { best = (double)d0; besti = idx0; }
-          if ((double)d1 > best) { best = (double)d1; besti = idx0 + 1; }
+        if (ARGMAX) {  // slots in increasing element order: strict > keeps the lowest index
+          if (d0 > bestv) { bestv = d0; besto = i; }
+          if (d1 > bestv) { bestv = d1; besto = i + 1; }
         }
       }
+      double best = (double)bestv;
+      long long besti = gbase + (long long)(((besto / VEC) * NTG + gtid) * VEC + (besto % VEC));
       PAM_TRACE(tr, 5 + 2 * t);
+      tok.give();
       const double2 r = cluster_reduce<NTG, ARGMAX>((double)sa + (double)sb, 0.0, best, besti, cb, xround, rank, C,
                                                     g, gtid);
       PAM_TRACE(tr, 6 + 2 * t);
@@ -497,10 +551,7 @@ __global__ void __launch_bounds__(NTG* G, (min_blocks_for<Elem, NTG * G, E>())) 
 
   const int64_t row0 = cid * G + g, rstride = ncl * G;
   uint32_t xround = 0, load_par = 0;
-  if (TMA && gtid == 0 && row0 < a.B) issue_load(row0);
-  // De-phase the row streams: identical clusters started together stay in
-  // lockstep and hit their HBM store bursts and exchanges at the same time.
-  // Row stream s = g*ncl + cid starts s/(G*ncl) of a row period late.
+  // De-phase the row streams (dev knob, default off).
   if (a.stagger > 0) {
     const long long wait = a.stagger * (long long)(g * ncl + cid) / (long long)(G * ncl);
     const long long t0 = clock64();
@@ -508,79 +559,146 @@ __global__ void __launch_bounds__(NTG* G, (min_blocks_for<Elem, NTG * G, E>())) 
   }
 
   Elem v[E];
+  // Register <- shared-memory slice copy (phantoms = k0).  Used for the first row.
+  auto lds_slice = [&](Elem k0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int li0 = (k * NTG + gtid) * VEC;
+      if (li0 + VEC <= len) {
+        const V t = *reinterpret_cast<const V*>(buf + li0);
+        *reinterpret_cast<V*>(&v[k * VEC]) = t;
+      } else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[k * VEC + j] = (li0 + j < len) ? buf[li0 + j] : k0;
+      }
+    }
+  };
 
-  for (int64_t row = row0; row < a.B; row += rstride) {
-    const int64_t lrow = (row - row0) / rstride;
-    long long* tr = (a.trace && g == 0 && lrow < kTraceRows)
-                        ? a.trace + ((int64_t)blockIdx.x * kTraceRows + lrow) * kTraceEvents
+  // TMA pipeline per group (landing buffer `buf`):
+  //   row r computes from registers while buf receives X(r+1);
+  //   at the end of row r each thread swaps Z(r) into buf and X(r+1) into its
+  //   registers, and one thread streams buf -> Z(r) with a bulk TMA store;
+  //   once that store has read buf (checked after the next row's first
+  //   exchange) the load of X(r+2) is issued into buf.
+  if (TMA && gtid == 0 && row0 < a.B) issue_load(row0);
+  if (TMA && row0 < a.B) {
+    ptx::mbar_wait_cta(bar_load, load_par);
+    load_par ^= 1u;
+    lds_slice(__ldg(X + row0 * a.ldx));
+    group_sync<NTG>(g);  // buf free
+  }
+  bool need_issue = TMA;  // deferred prefetch of the row after next
+
+  // Row slots: both groups of a CTA walk the same number of slots so their pass
+  // tokens stay balanced (a group without a row in its last slot idles).
+  const int64_t first0 = cid * G;
+  const int64_t K = (a.B > first0) ? (a.B - first0 + rstride - 1) / rstride : 0;
+  PassToken<NTG, G> tok(g, K * (int64_t)(T + 1));
+  for (int64_t k = 0; k < K; ++k) {
+    const int64_t row = row0 + k * rstride;
+    if (row >= a.B) {  // idle slot: keep the token moving
+      for (int ph = 0; ph <= T; ++ph) {
+        tok.take();
+        tok.give();
+      }
+      continue;
+    }
+    const int64_t next = row + rstride;
+    const bool has_next = next < a.B;
+    const int64_t lrow = k;
+    // trace: group g uses rows [g*kTraceRows/G, (g+1)*kTraceRows/G) of its CTA's trace block
+    long long* tr = (a.trace && lrow < kTraceRows / G)
+                        ? a.trace + ((int64_t)blockIdx.x * kTraceRows + g * (kTraceRows / G) + lrow) * kTraceEvents
                         : nullptr;
     PAM_TRACE(tr, 0);
     const Elem* xrow = X + row * a.ldx;
     const Elem k0e = __ldg(xrow);  // shift for the input pass (same in every CTA)
     const double K0 = (double)k0e;
-    group_sync<NTG>(g);  // previous row fully retired (wred / cand reuse)
+    const Elem k0next = has_next ? __ldg(X + next * a.ldx) : Elem(0);
+    tok.take();  // input pass (shift + moments) needs the fp64 pipe
 
-    // ---- load the slice into registers --------------------------------------
-    if (TMA) {
-      ptx::mbar_wait_cta(bar_load, load_par);
-      load_par ^= 1u;
-      PAM_TRACE(tr, 1);
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int li0 = (k * NTG + gtid) * VEC;
-        if (li0 + VEC <= len) {
-          const V t = *reinterpret_cast<const V*>(buf + li0);
-          *reinterpret_cast<V*>(&v[k * VEC]) = t;
-        } else {
-#pragma unroll
-          for (int j = 0; j < VEC; ++j) v[k * VEC + j] = (li0 + j < len) ? buf[li0 + j] : k0e;  // phantoms = K0
-        }
-      }
-      group_sync<NTG>(g);  // landing buffer free: prefetch the next row of this group
-      if (gtid == 0 && row + rstride < a.B) issue_load(row + rstride);
-      PAM_TRACE(tr, 2);
-    } else {
+    if (!TMA) {  // unaligned rows: direct loads, no staging
       const Elem* src = xrow + base;
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int li0 = (k * NTG + gtid) * VEC;
+      for (int kk = 0; kk < NV; ++kk) {
+        const int li0 = (kk * NTG + gtid) * VEC;
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) v[k * VEC + j] = (li0 + j < len) ? __ldcs(src + li0 + j) : k0e;
+        for (int j = 0; j < VEC; ++j) v[kk * VEC + j] = (li0 + j < len) ? __ldcs(src + li0 + j) : k0e;
       }
     }
+    PAM_TRACE(tr, 2);
+
+    // deferred: once the previous Z store has read buf, prefetch X(next) into it
+    auto prefetch_next = [&]() {
+      if (need_issue && gtid == 0) {
+        ptx::bulk_wait_read_all();
+        if (has_next) issue_load(next);
+      }
+    };
 
     // ---- input statistics + T CutMax iterations + normaliser + argmax ------------
     double rnorm = 1.0;
     long long amax = -1;
-    const int st = cutmax_core<Elem, NTG, E, P, true>(
-        v, K0, mphantom, rp, a.inv_n, cb, xround, rank, C, g, gtid, base,
-        (rank == 0 && gtid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr, rnorm, amax, tr);
+    const int st = cutmax_core<Elem, NTG, G, E, P, true>(
+        v, tok, K0, mphantom, rp, a.inv_n, cb, xround, rank, C, g, gtid, base,
+        (rank == 0 && gtid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr, rnorm, amax, tr, prefetch_next);
     PAM_TRACE(tr, 20);
     if (rank == 0 && gtid == 0) {
       if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)amax : -1;
       if (a.status) a.status[row] = st;
     }
 
-    // ---- Z = Y * inv(sum Y), streamed out with 128-bit evict-first stores -------
+    // ---- Z = Y * inv(sum Y) ------------------------------------------------------
     const Elem re = (Elem)rnorm;
     Elem* zrow = Z + row * a.ldz + base;
-    if (!(a.debug_flags & 1))
+    if (TMA) {
+      // swap: Z(row) -> buf, X(next) -> registers; then bulk-store buf -> Z(row)
+      if (has_next) {
+        ptx::mbar_wait_cta(bar_load, load_par);
+        load_par ^= 1u;
+      }
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const int li0 = (k * NTG + gtid) * VEC;
-      Elem o[VEC];
+      for (int kk = 0; kk < NV; ++kk) {
+        const int li0 = (kk * NTG + gtid) * VEC;
+        Elem o[VEC];
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) o[j] = v[k * VEC + j] * re;
-      if (TMA && li0 + VEC <= len) {
-        __stcs(reinterpret_cast<V*>(zrow + li0), *reinterpret_cast<V*>(o));
-      } else {
+        for (int j = 0; j < VEC; ++j) o[j] = v[kk * VEC + j] * re;
+        if (li0 + VEC <= len) {
+          const V xn = *reinterpret_cast<const V*>(buf + li0);
+          *reinterpret_cast<V*>(buf + li0) = *reinterpret_cast<V*>(o);
+          *reinterpret_cast<V*>(&v[kk * VEC]) = xn;
+        } else {
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) {
+            const Elem xn = (li0 + j < len) ? buf[li0 + j] : k0next;
+            if (li0 + j < len) buf[li0 + j] = o[j];
+            v[kk * VEC + j] = xn;
+          }
+        }
+      }
+      ptx::fence_proxy_async_smem();  // make the Z writes visible to the TMA engine
+      group_sync<NTG>(g);
+      if (gtid == 0 && !(a.debug_flags & 1)) {
+        const uint32_t zbytes = load_bytes;
+        const unsigned char* dstb = reinterpret_cast<const unsigned char*>(zrow);
+        for (uint32_t off = 0; off < zbytes; off += 32768u) {
+          const uint32_t nb = (zbytes - off) < 32768u ? (zbytes - off) : 32768u;
+          ptx::bulk_s2g((void*)(dstb + off), ptx::smem_addr(buf) + off, nb, policy);
+        }
+        ptx::bulk_commit();
+      }
+    } else if (!(a.debug_flags & 1)) {
+#pragma unroll
+      for (int kk = 0; kk < NV; ++kk) {
+        const int li0 = (kk * NTG + gtid) * VEC;
 #pragma unroll
         for (int j = 0; j < VEC; ++j)
-          if (li0 + j < len) __stcs(zrow + li0 + j, o[j]);
+          if (li0 + j < len) __stcs(zrow + li0 + j, v[kk * VEC + j] * re);
       }
     }
     PAM_TRACE(tr, 21);
   }
+  if (TMA && gtid == 0) ptx::bulk_wait_all();  // Z stores complete before the CTA retires
   ptx::cluster_sync();  // no CTA leaves while a peer may still push into its shared memory
 }
 

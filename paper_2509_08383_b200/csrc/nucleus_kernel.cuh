@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
 
     double rnorm = 1.0;
     long long unused_argmax;
-    int st = cutmax_core<double, NT, E, P, false>(v, K0, mphantom, a.rp, a.inv_n, cb, xround, rank, C, 0, tid, base,
+    PassToken<NT, 1> tok(0, 0);
+    int st = cutmax_core<double, NT, 1, E, P, false>(v, tok, K0, mphantom, a.rp, a.inv_n, cb, xround, rank, C, 0, tid, base,
                                                   nullptr, rnorm, unused_argmax);
 
     // token candidate over Z = Y * rnorm (and optional one-hot store)

@@ -63,6 +63,19 @@ Geometry choose_geometry(int elem_bytes, int64_t B, int64_t n) {
     }
   }
   (void)B;
+  // Measured preferences (tools/tune.py on B200): per-CTA slices of 256x76
+  // fp32 (two CTAs per SM) beat 512x40 (one per SM) for rows of >= 64K floats.
+  if (elem_bytes == 4 && n >= 65536) {
+    for (int i = 0; i < kNumCutmaxVariants; ++i) {
+      const Variant& v = kCutmaxVariants[i];
+      if (v.elem_bytes == 4 && v.ntg == 256 && v.e == 76 && v.g == 1) {
+        for (int C = 1; C <= 16; C *= 2) {
+          const int64_t L = slice_len(n, C, vec);
+          if ((int64_t)v.ntg * v.e >= L) { g.var = &v; g.C = C; g.L = (int)L; return g; }
+        }
+      }
+    }
+  }
   for (int C = 1; C <= 16; C *= 2) {
     const int64_t L = slice_len(n, C, vec);
     const Variant* best = nullptr;

@@ -299,10 +299,11 @@ def test_spec_known_answers_on_gpu(cuda, pam, orc):
         assert abs(z[0] - sstar) <= 1e-12
 
 
-@pytest.mark.parametrize("geom", ["128,8,16", "256,16,4", "512,16,8", "512,24,2", "512,38,1"])
+@pytest.mark.parametrize("geom", ["128,8,16", "256,16,4", "512,16,8", "512,24,2", "512,38,1",
+                                  "256,38,16,2", "256,16,4,2", "128,8,2,2", "256,24,8,2"])
 def test_forced_geometries(cuda, pam, orc, geom):
     """Every cluster size 1..16 through the env override."""
-    x = W.gaussian(20, 9000, seed=17)
+    x = W.gaussian(21, 9000, seed=17)  # odd B: a row group idles in its last slot
     prm = pam.CutMaxParams()
     os.environ["PAM_FORCE_CFG_F64"] = geom
     try:

@@ -37,7 +37,7 @@ def run(B, n, dtype, cfg=None):
         print(f"   {NAMES.get(b, b):28s} {v:8.0f} cyc  {v/1.965e3:7.2f} us  {100*v/tot:5.1f}%")
     print(f"   {'gap to next row':28s} {np.median(nxt):8.0f} cyc")
     for a, b, nm in ((3, 24, "xchg0: warp tree + push"), (24, 25, "xchg0: mbarrier wait"), (25, 26, "xchg0: slot reduce"),
-                     (26, 4, "xchg0: return"), (4, 27, "scalar math (iter0)")):
+                     (26, 4, "xchg0: return"), (4, 28, "  guard"), (28, 29, "  loop top/status"), (29, 30, "  invsqrt"), (30, 27, "  k, b"), (4, 27, "scalar math (iter0)")):
         print(f"   {nm:28s} {np.median(rows[:, :, b] - rows[:, :, a]):8.0f} cyc")
     sk = tr[:, 1:7, 24].reshape(-1, info['cluster'], 6) if False else None
     print(f"   {'row period':28s} {tot:8.0f} cyc  {tot/1.965e3:7.2f} us")
@@ -45,6 +45,7 @@ def run(B, n, dtype, cfg=None):
 
 run(4096, 151936, torch.float64)
 run(4096, 151936, torch.float64, "256,38,16,2")
+run(4096, 32768, torch.float64, "256,38,4,2")
 run(4096, 32768, torch.float64)
 run(4096, 151936, torch.float32)
 run(4096, 1024, torch.float64)
