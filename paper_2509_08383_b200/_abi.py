@@ -99,7 +99,7 @@ SIGNATURES = {
 }
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libpam.so")
+LIB_PATH = os.environ.get("PAM_LIB_PATH") or os.path.join(PKG_DIR, "libpam.so")  # override: dev trace build
 
 _lib = None
 

@@ -4,14 +4,9 @@
 //
 // Geometry.  One logit row is owned by one thread-block cluster of C CTAs
 // (C = 1..16).  CTA `rank` owns the contiguous slice [rank*L, min(n,(rank+1)*L)).
-// A CTA runs G independent "row groups" of NTG threads each (named barriers
-// 1..G, own mbarriers, own landing buffer): group g of cluster c processes rows
-// c*G + g, c*G + g + ncl*G, ...  While one group sits in a cluster exchange or
-// streams its Z out, the other group's fp64 passes keep the SM busy.
-// Each thread of a group keeps E elements of its slice in registers for all T
-// iterations: HBM is read once (1-D TMA bulk copy into the group's shared
-// memory landing buffer, prefetched one row ahead) and written once (128-bit
-// streaming stores).
+// Each of the NTG threads keeps E elements of the slice in registers for all T
+// iterations: HBM is read once (1-D TMA bulk copy into the CTA's shared-memory
+// row buffer, prefetched one row ahead) and written once (TMA bulk store).
 //
 // Reductions.  Every iteration needs the row mean and variance.  Values are
 // stored shifted, v = y - K, with a shift K shared by every CTA (K = x[0] for
@@ -23,12 +18,26 @@
 // the kernel does an exact second pass sum((v-dm)^2) and a second exchange;
 // the decision is cluster-uniform because every CTA holds identical sums.
 //
-// Exchange.  Each warp butterfly-reduces its lanes and pushes its partial into
-// slot (rank, warp) of every CTA of the cluster with st.async (DSMEM),
-// completing on the destination group's mbarrier; every warp then sums the
-// same C*NW slots in the same order.  xor-butterflies leave bit-identical sums
-// in every lane (IEEE addition is commutative), so all CTAs compute identical
-// mu and s2 without a broadcast.  The argmax candidate is gathered to rank 0.
+// Exchange.  Each warp butterfly-reduces its lanes into a per-warp partial;
+// after a CTA barrier warp 0 combines the partials and pushes ONE 32-byte
+// record (sums + argmax candidate) into slot [rank] of every CTA of the
+// cluster with st.async (DSMEM), completing on the destination's mbarrier;
+// every warp then combines the C records in the same butterfly order.
+// xor-butterflies leave bit-identical values in every lane (IEEE addition is
+// commutative), so all CTAs compute identical mu and s2 without a broadcast.
+//
+// Row pipeline (TMA path).  Per row, T exchanges — the input statistics ride
+// on the previous row's last exchange:
+//   pass t (t < T-1): update + moments            -> exchange t
+//   pass T-1: Y^(T+1), sum Y, argmax             -> push (no wait)
+//   swap: unnormalised Y(r) -> row buffer, X(r+1) - K0(r+1) -> registers,
+//         moments of X(r+1)                       -> push; wait both
+//   row r+1, pass 0 also scales the buffer by inv(sum Y(r)) = Z(r); the DMA
+//   thread then streams Z(r) out (4 bulk-store chunks) and, chunk by chunk as
+//   the store has read them, streams X(r+2) in.
+// Normalising one pass late lets the row-boundary exchange carry both rows,
+// and the prologue's input pass + exchange is needed only for a cluster's
+// first row.
 //
 // Element update (z = (y-mu)/(c sigma) + 1, y' = z^p):
 //     z = fma(v, k, b)  with k = inv_sigma/c, b = 1 - dm*k
@@ -64,14 +73,12 @@ struct CutmaxArgs {
   int32_t* status;
   double* stats;
   int64_t ldx, ldz, B, n;
-  int32_t L;             // slice length per CTA (elements)
-  int32_t buf_bytes;     // landing-buffer bytes per group (0 without TMA)
-  int32_t ctrl_offset;   // byte offset of the first group's control block
-  int32_t tma;           // 1: TMA bulk loads + 128-bit stores (16-byte aligned rows), 0: scalar path
-  double inv_n;          // 1/n
-  long long* trace;      // debug: per-CTA phase timestamps (pam_set_trace_buffer), normally null
-  int64_t stagger;       // start offset (SM cycles) spread over clusters / groups to de-phase them
-  int32_t debug_flags;   // dev experiments: 1 = skip Z stores
+  int32_t L;            // slice length per CTA (elements)
+  int32_t ctrl_offset;  // byte offset of the control block (after the row buffer)
+  int32_t tma;          // 1: TMA bulk loads/stores (16-byte aligned rows), 0: direct loads/stores
+  int32_t debug_flags;  // dev experiments: 1 = skip Z stores
+  double inv_n;         // 1/n
+  long long* trace;     // debug: per-CTA phase timestamps (pam_set_trace_buffer), normally null
   RowParams rp;
 };
 
@@ -84,21 +91,38 @@ struct __align__(16) XchRecord {
 
 struct __align__(16) ControlBlock {
   XchRecord xch[2][16];  // exchange slots per cluster rank, double-buffered by round parity
+  double2 xin[16];       // next row's input sums per cluster rank (row-boundary exchange)
   double2 wred[32];      // per-warp partial sums (CTA pre-reduction; sampler token gather)
   double2 wcand[32];     // per-warp argmax candidates
+  double2 wred2[32];     // per-warp partials of the next row's input sums
   double2 gat[16][2];    // all-gather records (sampler: token candidate + max x)
   unsigned long long mb_load;
   unsigned long long mb_x[2];
   unsigned long long mb_g;
+  unsigned long long mb_in;
 };
 
-// Debug phase tracing: thread 0 of group 0 of each CTA stamps clock64() at
-// phase boundaries of its first kTraceRows rows (tools/trace.py reads them).
+// Debug phase tracing (builds with -DPAM_TRACE_BUILD only; tools/trace.py):
+// thread 0 of each CTA stamps clock64() at phase boundaries of its first
+// kTraceRows rows.  Compiled out otherwise so it costs no registers.
 constexpr int kTraceRows = 8, kTraceEvents = 32;
+#ifdef PAM_TRACE_BUILD
 #define PAM_TRACE(tr, k)                                   \
   do {                                                     \
     if ((tr) != nullptr && gtid == 0) (tr)[k] = clock64(); \
   } while (0)
+#define PAM_TRACE_DMA(tr, k)                 \
+  do {                                       \
+    if ((tr) != nullptr) (tr)[k] = clock64(); \
+  } while (0)
+#else
+#define PAM_TRACE(tr, k) \
+  do {                   \
+  } while (0)
+#define PAM_TRACE_DMA(tr, k) \
+  do {                       \
+  } while (0)
+#endif
 
 template <typename T>
 struct ElemTraits;
@@ -118,59 +142,14 @@ __device__ __forceinline__ float fma_e(float a, float b, float c) { return fmaf(
 __device__ __forceinline__ double ipow_e(double z, int p) { return ipow(z, p); }
 __device__ __forceinline__ float ipow_e(float z, int p) { return ipowf(z, p); }
 
-// Named barrier for the NTG threads of group g (barrier 0 is __syncthreads).
-template <int NTG>
-__device__ __forceinline__ void group_sync(int g) {
-  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(NTG) : "memory");
-}
-
-// Strict alternation of the fp64 element passes of the G=2 row groups of a CTA.
-// A group holds the token while it streams its slice through the fp64 pipe and
-// hands it over before waiting in its cluster exchange, so one group's
-// exchange latency overlaps the other group's pass.  Named barrier 3+g carries
-// the token to group g (the giver arrives, the taker syncs: 2*NTG threads).
-// Group 0 starts with the token; every group takes and gives exactly
-// K*(T+1) times except that group 0 skips its first take and group 1 its last
-// give, which keeps the barrier arrivals balanced.  G=1: no-ops.
-template <int NTG, int G>
-struct PassToken {
-  int g;
-  int64_t left;  // gives still to perform
-  bool skip_take;
-  __device__ __forceinline__ PassToken(int g_, int64_t total) : g(g_), left(total - (g_ == 1 ? 1 : 0)), skip_take(g_ == 0) {}
-  __device__ __forceinline__ void take() {
-    if (G == 2) {
-      if (skip_take) {
-        skip_take = false;
-      } else {
-        asm volatile("bar.sync %0, %1;" ::"r"(3 + g), "r"(2 * NTG) : "memory");
-      }
-    }
-  }
-  __device__ __forceinline__ void give() {
-    if (G == 2 && left > 0) {
-      --left;
-      asm volatile("bar.arrive %0, %1;" ::"r"(3 + (g ^ 1)), "r"(2 * NTG) : "memory");
-    }
-  }
-};
-
-__device__ __forceinline__ void butterfly_sum2(double& a, double& b) {
-#pragma unroll
-  for (int m = 16; m > 0; m >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, m);
-    b += __shfl_xor_sync(0xffffffffu, b, m);
-  }
-}
-
 __device__ __forceinline__ bool cand_better(double v, long long i, double bv, long long bi) {
   return (v > bv) || (v == bv && i < bi);
 }
 
-// xor-butterfly over the low `width` lanes' groups (width a power of two <= 32):
-// every lane ends with the combination of its aligned width-group, and because
-// IEEE addition / the argmax rule are commutative, all lanes of a group hold
-// bit-identical values.
+// xor-butterfly over aligned WIDTH-lane groups (WIDTH a power of two <= 32):
+// every lane ends with the combination of its group, and because IEEE addition
+// and the argmax rule are commutative, all lanes of a group hold bit-identical
+// values.
 template <int WIDTH>
 __device__ __forceinline__ void bfly_sum2(double& a, double& b) {
 #pragma unroll
@@ -193,84 +172,178 @@ __device__ __forceinline__ void bfly_argmax(double& best, long long& besti) {
   }
 }
 
-__device__ __forceinline__ void butterfly_argmax(double& best, long long& besti) { bfly_argmax<32>(best, besti); }
-
 // ---------------------------------------------------------------------------
-// Cluster-wide reduction over one row group: sums of (a, b) and, when ARGMAX,
-// the lexicographic (value desc, index asc) maximum of (best, besti).  All NTG
-// threads of group g must call it; every thread returns the cluster result,
-// bit-identical in every CTA.
-//   warp butterfly -> per-warp partial in smem -> named barrier -> warp 0
-//   combines the NW partials and pushes one 32-byte record into slot [rank] of
-//   every CTA (st.async, complete_tx on the destination's mbarrier) -> every
-//   warp combines the C records in the same fixed butterfly order.
-template <int NTG, bool ARGMAX>
-__device__ __forceinline__ double2 cluster_reduce(double a, double b, double& best, long long& besti, ControlBlock* cb,
-                                                  uint32_t& round, uint32_t rank, uint32_t C, int g, int gtid,
-                                                  long long* tr = nullptr) {
+// Cluster exchange, split in two so independent work can run between the push
+// and the wait.  All NTG threads of the CTA call both halves.
+//
+// xch_push: warp butterfly -> per-warp partial in smem -> CTA barrier -> warp 0
+// combines the NW partials and pushes one 32-byte record into slot [rank] of
+// every CTA (st.async, complete_tx on the destination's mbarrier).  `side` runs
+// on lane 0 of the last warp right after the barrier (the DMA thread's hook:
+// bulk stores / loads issued there stay off warp 0's critical path).
+struct NoSide {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// Exchange payloads: two sums; three sums (the third rides in the candidate
+// slot); or two sums plus the lexicographic (value desc, index asc) argmax.
+enum XchMode { kSum2 = 0, kSum3 = 1, kArgmax = 2 };
+
+template <int NTG, int MODE, typename Side = NoSide>
+__device__ __forceinline__ void xch_push(double a, double b, double c, long long ci_, ControlBlock* cb,
+                                         const uint32_t round, const uint32_t rank, const uint32_t C, const int gtid,
+                                         const Side& side = Side()) {
   constexpr int NW = NTG / 32;
   const int lane = gtid & 31, warp = gtid >> 5;
+  double c2 = 0.0;  // unused partner of c in kSum3 (keeps the butterfly a pair)
+  long long ci = ci_;
   bfly_sum2<32>(a, b);
-  if (ARGMAX) bfly_argmax<32>(best, besti);
+  if (MODE == kArgmax) bfly_argmax<32>(c, ci);
+  if (MODE == kSum3) bfly_sum2<32>(c, c2);
   if (lane == 0) {
     cb->wred[warp] = make_double2(a, b);
-    if (ARGMAX) cb->wcand[warp] = make_double2(best, __longlong_as_double(besti));
+    if (MODE != kSum2) cb->wcand[warp] = make_double2(c, __longlong_as_double(ci));
   }
-  group_sync<NTG>(g);
-  const uint32_t par = round & 1u, ph = (round >> 1) & 1u;
+  __syncthreads();
+  const uint32_t par = round & 1u;
   if (warp == 0) {
     const double2 w = cb->wred[lane & (NW - 1)];
     double ca = w.x, cbv = w.y;
     bfly_sum2<NW>(ca, cbv);
     double cv = -HUGE_VAL;
-    long long ci = 0x7fffffffffffffffLL;
-    if (ARGMAX) {
+    long long cix = 0x7fffffffffffffffLL;
+    if (MODE != kSum2) {
       const double2 wc = cb->wcand[lane & (NW - 1)];
       cv = wc.x;
-      ci = __double_as_longlong(wc.y);
-      bfly_argmax<NW>(cv, ci);
+      cix = __double_as_longlong(wc.y);
+      if (MODE == kArgmax) bfly_argmax<NW>(cv, cix);
+      if (MODE == kSum3) {
+        double z = 0.0;
+        bfly_sum2<NW>(cv, z);
+      }
     }
     if (lane < (int)C) {
       const uint32_t bar = ptx::mapa(ptx::smem_addr(&cb->mb_x[par]), (uint32_t)lane);
       ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->xch[par][rank].ab), (uint32_t)lane), ca, cbv, bar);
       ptx::st_async_b64x2(ptx::mapa(ptx::smem_addr(&cb->xch[par][rank].cand), (uint32_t)lane),
-                          (uint64_t)__double_as_longlong(cv), (uint64_t)ci, bar);
+                          (uint64_t)__double_as_longlong(cv), (uint64_t)cix, bar);
     }
+  } else if (warp == NW - 1 && lane == 0) {
+    side();
   }
-  PAM_TRACE(tr, 24);
+}
+
+// xch_wait: wait for the C records of this round, re-arm the barrier for
+// round + 2 and combine the records (16-lane butterfly, same order everywhere).
+// Returns (a, b); c / ci receive the third sum or the argmax.
+template <int MODE>
+__device__ __forceinline__ double2 xch_wait(double& c, long long& ci, ControlBlock* cb, uint32_t& round,
+                                            const uint32_t C, const int gtid) {
+  const int lane = gtid & 31;
+  const uint32_t par = round & 1u, ph = (round >> 1) & 1u;
   ptx::mbar_wait_cta(ptx::smem_addr(&cb->mb_x[par]), ph);
-  PAM_TRACE(tr, 25);
   if (gtid == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[par]), C * 32u);  // arm round+2
   const int src = lane & 15;
   const bool have = src < (int)C;
   const XchRecord rec = cb->xch[par][have ? src : 0];
-  a = have ? rec.ab.x : 0.0;
-  b = have ? rec.ab.y : 0.0;
+  double a = have ? rec.ab.x : 0.0;
+  double b = have ? rec.ab.y : 0.0;
   bfly_sum2<16>(a, b);
-  if (ARGMAX) {
-    best = have ? rec.cand.x : -HUGE_VAL;
-    besti = have ? __double_as_longlong(rec.cand.y) : 0x7fffffffffffffffLL;
-    bfly_argmax<16>(best, besti);
+  if (MODE == kArgmax) {
+    c = have ? rec.cand.x : -HUGE_VAL;
+    ci = have ? __double_as_longlong(rec.cand.y) : 0x7fffffffffffffffLL;
+    bfly_argmax<16>(c, ci);
   }
-  PAM_TRACE(tr, 26);
+  if (MODE == kSum3) {
+    c = have ? rec.cand.x : 0.0;
+    double z = 0.0;
+    bfly_sum2<16>(c, z);
+  }
   ++round;
   return make_double2(a, b);
 }
 
+template <int NTG, bool ARGMAX>
+__device__ __forceinline__ double2 cluster_reduce(double a, double b, double& best, long long& besti, ControlBlock* cb,
+                                                  uint32_t& round, const uint32_t rank, const uint32_t C,
+                                                  const int gtid) {
+  constexpr int M = ARGMAX ? kArgmax : kSum2;
+  xch_push<NTG, M>(a, b, best, besti, cb, round, rank, C, gtid);
+  return xch_wait<M>(best, besti, cb, round, C, gtid);
+}
+
 template <int NTG>
-__device__ __forceinline__ double2 cluster_sum2(double a, double b, ControlBlock* cb, uint32_t& round, uint32_t rank,
-                                                uint32_t C, int g, int gtid, long long* tr = nullptr) {
+__device__ __forceinline__ double2 cluster_sum2(double a, double b, ControlBlock* cb, uint32_t& round,
+                                                const uint32_t rank, const uint32_t C, const int gtid) {
   double bv = 0.0;
   long long bi = 0;
-  return cluster_reduce<NTG, false>(a, b, bv, bi, cb, round, rank, C, g, gtid, tr);
+  return cluster_reduce<NTG, false>(a, b, bv, bi, cb, round, rank, C, gtid);
+}
+
+// Three cluster sums in one exchange.
+template <int NTG>
+__device__ __forceinline__ double3 cluster_sum3(double a, double b, double c, ControlBlock* cb, uint32_t& round,
+                                                const uint32_t rank, const uint32_t C, const int gtid) {
+  long long ci = 0;
+  xch_push<NTG, kSum3>(a, b, c, ci, cb, round, rank, C, gtid);
+  const double2 r = xch_wait<kSum3>(c, ci, cb, round, C, gtid);
+  return make_double3(r.x, r.y, c);
+}
+
+// Next row's input sums (row-boundary exchange, second record): own per-warp
+// slots, own records and mbarrier (mb_in, one phase per row).
+template <int NTG>
+__device__ __forceinline__ void xin_push(double s, double q, ControlBlock* cb, const uint32_t rank, const uint32_t C,
+                                         const int gtid) {
+  constexpr int NW = NTG / 32;
+  const int lane = gtid & 31, warp = gtid >> 5;
+  bfly_sum2<32>(s, q);
+  if (lane == 0) cb->wred2[warp] = make_double2(s, q);
+  __syncthreads();
+  if (warp == 0) {
+    const double2 w = cb->wred2[lane & (NW - 1)];
+    double cs = w.x, cq = w.y;
+    bfly_sum2<NW>(cs, cq);
+    if (lane < (int)C) {
+      const uint32_t bar = ptx::mapa(ptx::smem_addr(&cb->mb_in), (uint32_t)lane);
+      ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->xin[rank]), (uint32_t)lane), cs, cq, bar);
+    }
+  }
+}
+
+__device__ __forceinline__ double2 xin_wait(ControlBlock* cb, uint32_t& in_par, const uint32_t C, const int gtid) {
+  const int lane = gtid & 31;
+  ptx::mbar_wait_cta(ptx::smem_addr(&cb->mb_in), in_par);
+  in_par ^= 1u;
+  if (gtid == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_in), C * 16u);  // arm the next row
+  const int src = lane & 15;
+  const bool have = src < (int)C;
+  const double2 rec = cb->xin[have ? src : 0];
+  double s = have ? rec.x : 0.0, q = have ? rec.y : 0.0;
+  bfly_sum2<16>(s, q);
+  return make_double2(s, q);
 }
 
 // ---------------------------------------------------------------------------
-// One element update z = fma(v, k, b), v' = z^p - K'.  Used for the register
+// The affine step z = (v - dm) * k + 1 of one element.
+//   fp64: z = fma(v, k, b) with b = 1 - dm*k (one instruction; b's rounding
+//         error 2^-53 stays far inside the 1e-12 tolerance after p^T growth).
+//   fp32: z = fma(v - dm, k, 1): rounding b to fp32 would put a 2^-24 offset
+//         into every z (amplified ~p^T), so dm is subtracted first, like the
+//         oracle's (z - mu) * k + 1 (oracle.c orc_cutmax_f32).
+// `b` is the per-type coefficient from affine_coef().
+__device__ __forceinline__ double affine_e(double v, double k, double b) { return fma(v, k, b); }
+__device__ __forceinline__ float affine_e(float v, float k, float dm) { return fmaf(v - dm, k, 1.0f); }
+template <typename Elem>
+__device__ __forceinline__ Elem affine_coef(double bd, double dm) {
+  return sizeof(Elem) == 8 ? (Elem)bd : (Elem)dm;
+}
+
+// One element update z = affine(v), v' = z^p - K'.  Used for the register
 // slice and for the scalar phantom trajectory, so both round identically.
 template <typename Elem, int P>
 __device__ __forceinline__ Elem cutmax_update(Elem v, Elem k, Elem b, Elem kn, int p) {
-  const Elem zz = fma_e(v, k, b);
+  const Elem zz = affine_e(v, k, b);
   if (P == 3) {
     const Elem z2 = zz * zz;
     return fma_e(z2, zz, kn);
@@ -284,35 +357,104 @@ __device__ __forceinline__ void moments_from_sums(double S, double Q, double inv
   s2 = fma(-dm, dm, Q * inv_n);
 }
 
+// Input pass: shift the slice by K0 in place and return this thread's
+// (sum v, sum v^2).  Phantom slots hold K0 and so contribute exactly 0.
+template <typename Elem, int E>
+__device__ __forceinline__ double2 input_pass(Elem (&v)[E], const double K0) {
+  const Elem k0 = (Elem)K0;
+  Elem sa = 0, sb = 0, qa = 0, qb = 0;
+#pragma unroll
+  for (int i = 0; i < E; i += 2) {
+    const Elem d0 = v[i] - k0, d1 = v[i + 1] - k0;
+    v[i] = d0;
+    v[i + 1] = d1;
+    sa += d0;
+    sb += d1;
+    qa = fma_e(d0, d0, qa);
+    qb = fma_e(d1, d1, qb);
+  }
+  return make_double2((double)sa + (double)sb, (double)qa + (double)qb);
+}
+
+// Input pass with the third power sum as well (the p = 3 analytic normaliser
+// needs the third central moment of the iterate feeding the last iteration;
+// for T = 1 that is the input).
+template <typename Elem, int E>
+__device__ __forceinline__ double3 input_pass3(Elem (&v)[E], const double K0) {
+  const Elem k0 = (Elem)K0;
+  Elem sa = 0, sb = 0, qa = 0, qb = 0, ra = 0, rb = 0;
+#pragma unroll
+  for (int i = 0; i < E; i += 2) {
+    const Elem d0 = v[i] - k0, d1 = v[i + 1] - k0;
+    v[i] = d0;
+    v[i + 1] = d1;
+    sa += d0;
+    sb += d1;
+    const Elem e0 = d0 * d0, e1 = d1 * d1;
+    qa += e0;
+    qb += e1;
+    ra = fma_e(e0, d0, ra);
+    rb = fma_e(e1, d1, rb);
+  }
+  return make_double3((double)sa + (double)sb, (double)qa + (double)qb, (double)ra + (double)rb);
+}
+
+// Hooks the caller threads into the iterations:
+//   pass0_on / pass0(kk): side work fused into the first pass, per vector slot kk
+//   side(e):               DMA hook, run inside exchange e's push (see xch_push)
+//   final_xch(sy, best, besti) -> raw cluster sum of Y^(T+1); performs the last
+//                          exchange (and whatever the caller overlaps with it)
+template <typename P0, typename SD, typename FX>
+struct IterHooks {
+  bool pass0_on;
+  P0 pass0;
+  SD side;
+  FX final_xch;
+};
+template <typename P0, typename SD, typename FX>
+__device__ __forceinline__ IterHooks<P0, SD, FX> make_hooks(bool on, P0 p0, SD sd, FX fx) {
+  return IterHooks<P0, SD, FX>{on, p0, sd, fx};
+}
+
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
+};
+template <int I>
+struct IntC {
+  static constexpr int value = I;
+};
+
 // ---------------------------------------------------------------------------
-// CutMax on a register-resident row slice (one row group).
+// CutMax iterations on a register-resident, K0-shifted row slice.
 //
-// On entry v[] holds the group's slice: `len` real elements followed by
-// phantom elements (slots beyond the slice) that the caller filled with K0.
-// Phantoms keep every pass free of per-element predicates: all phantoms of the
-// row carry one common value w_t (they start at K0 and get the same updates),
-// tracked here as a scalar, and their total contribution m*w (m = number of
-// phantoms in the cluster) is subtracted from the cluster sums.
+// (S_in, Q_in) are the cluster sums of the shifted input.  `len` real elements
+// are followed by phantom slots (beyond the slice) that start as copies of
+// element 0 (0 in the shifted representation) and get the same updates, so the
+// element passes need no per-element control flow.  All phantoms of the row
+// carry one common value w_t, tracked as a scalar, and
+//   fp64: their total contribution mph*w (mph = phantom slots in the cluster)
+//         is subtracted from the cluster sums — no predicate in the passes;
+//   fp32: they are left out of the sums by a per-slot predicate (mph = 0): the
+//         fp32 partial sums would round the mph identical terms coherently,
+//         ~1e-6 relative in the variance and ~1e-5 in Z after p^T growth.
 //
 // With ARGMAX, the last iteration's pass also tracks the argmax of Y^(T+1)
 // (pin A7: equals argmax Z for the positive normaliser) and the last exchange
-// carries it, so no separate gather is needed.  When the caller filled the
-// phantoms with x[0] and K0 = x[0], phantoms are exact copies of element 0 and
-// can never beat it (equal value, larger index), so no predicate is needed.
+// carries it.  Phantoms are exact copies of element 0 (shift K0 = x[0]), so
+// they can never beat it (equal value, larger index): no predicate needed.
 //
-// On exit v holds Y^(T+1) (shift 0) and rnorm the normaliser inv(sum Y) (1
-// when PAM_F_NO_NORMALIZE).  Returns the row status, identical in every CTA.
-struct NoOp {
-  __device__ __forceinline__ void operator()() const {}
-};
-
-template <typename Elem, int NTG, int G, int E, int P, bool ARGMAX, typename AfterFirstXchg = NoOp>
-__device__ __forceinline__ int cutmax_core(Elem (&v)[E], PassToken<NTG, G>& tok, const double K0, const double mphantom,
-                                           const RowParams& rp, const double inv_n, ControlBlock* cb,
-                                           uint32_t& xround, const uint32_t rank, const uint32_t C, const int g,
-                                           const int gtid, const int64_t gbase, double* stats_row, double& rnorm,
-                                           long long& argmax_out, long long* tr = nullptr,
-                                           const AfterFirstXchg& after_first_xchg = AfterFirstXchg()) {
+// On exit rnorm is the normaliser inv(sum Y) (1 when PAM_F_NO_NORMALIZE).
+// v holds Y^(T+1) unless final_xch reused the registers.  Returns the row
+// status, identical in every CTA.
+template <typename Elem, int NTG, int E, int P, bool ARGMAX, typename Hooks>
+__device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, const double Q_in, const double K0,
+                                              const int len, const double mph, const RowParams& rp,
+                                              const double inv_n,
+                                              ControlBlock* cb, uint32_t& xround, const uint32_t rank,
+                                              const uint32_t C, const int gtid, const int64_t gbase,
+                                              double* stats_row, double& rnorm, long long& argmax_out, Hooks& h,
+                                              long long* tr) {
   using Tr = ElemTraits<Elem>;
   constexpr int VEC = Tr::VEC;
   constexpr double kGuard = sizeof(Elem) == 8 ? 16.0 : 2.0;  // cancellation guard (see header)
@@ -325,6 +467,8 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], PassToken<NTG, G>& tok,
   int st = PAM_OK;
   rnorm = 1.0;
   argmax_out = -1;
+  // slot i holds an element (fp32 only; fp64 corrects by mph * w instead)
+  auto real = [&](int i) { return sizeof(Elem) == 8 || ((i / VEC) * NTG + gtid) * VEC + (i % VEC) < len; };
 
   // exact second pass about dm when the shifted one-pass moments cancelled
   auto guard = [&](double S, double Q, double w, double& dm, double& s2) {
@@ -335,12 +479,12 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], PassToken<NTG, G>& tok,
 #pragma unroll
       for (int i = 0; i < E; i += 2) {
         const Elem d0 = v[i] - dme, d1 = v[i + 1] - dme;
-        q2a = fma_e(d0, d0, q2a);
-        q2b = fma_e(d1, d1, q2b);
+        if (real(i)) q2a = fma_e(d0, d0, q2a);
+        if (real(i + 1)) q2b = fma_e(d1, d1, q2b);
       }
-      const double2 r2 = cluster_sum2<NTG>((double)q2a + (double)q2b, 0.0, cb, xround, rank, C, g, gtid);
+      const double2 r2 = cluster_sum2<NTG>((double)q2a + (double)q2b, 0.0, cb, xround, rank, C, gtid);
       const Elem dw = (Elem)w - dme;
-      s2 = (r2.x - mphantom * (double)dw * (double)dw) * inv_n;
+      s2 = (r2.x - mph * (double)dw * (double)dw) * inv_n;
     }
   };
 
@@ -348,33 +492,39 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], PassToken<NTG, G>& tok,
   double c_inv = rp.inv_c[0], knext = rp.kshift[1];
   int pcur = rp.p[0];
 
-  // ---- input pass: shift by K0 (phantoms hold K0 -> contribute exactly 0) ---
   double dm, s2;
-  {
-    const Elem k0 = (Elem)K0;
-    Elem sa = 0, sb = 0, qa = 0, qb = 0;
-#pragma unroll
-    for (int i = 0; i < E; i += 2) {
-      const Elem d0 = v[i] - k0, d1 = v[i + 1] - k0;
-      v[i] = d0;
-      v[i + 1] = d1;
-      sa += d0;
-      sb += d1;
-      qa = fma_e(d0, d0, qa);
-      qb = fma_e(d1, d1, qb);
-    }
-    PAM_TRACE(tr, 3);
-    tok.give();
-    const double2 r =
-        cluster_sum2<NTG>((double)sa + (double)sb, (double)qa + (double)qb, cb, xround, rank, C, g, gtid, tr);
-    PAM_TRACE(tr, 4);
-    if (T == 1) after_first_xchg();
-    if (!isfinite(r.x) || !isfinite(r.y)) st = PAM_ERR_NON_FINITE;
-    guard(r.x, r.y, 0.0, dm, s2);
-    PAM_TRACE(tr, 28);
-  }
+  if (!isfinite(S_in) || !isfinite(Q_in)) st = PAM_ERR_NON_FINITE;
+  guard(S_in, Q_in, 0.0, dm, s2);
+  PAM_TRACE(tr, 4);
   double kcur = K0;
   Elem w = 0;  // phantom value (shifted representation)
+
+  // one element pass; FIRST: fused pass-0 side work, LAST: argmax, no moments
+  auto pass = [&](auto first_c, auto last_c, Elem ke, Elem be, Elem kn, int p, Elem& sa, Elem& sb, Elem& qa,
+                  Elem& qb, Elem& bestv, int& besto) {
+    constexpr bool FIRST = decltype(first_c)::value, LAST = decltype(last_c)::value;
+#pragma unroll
+    for (int i = 0; i < E; i += 2) {
+      if (FIRST && (i % VEC) == 0) h.pass0(i / VEC);
+      const Elem d0 = cutmax_update<Elem, P>(v[i], ke, be, kn, p);
+      const Elem d1 = cutmax_update<Elem, P>(v[i + 1], ke, be, kn, p);
+      v[i] = d0;
+      v[i + 1] = d1;
+      if (real(i)) {
+        sa += d0;
+        if (!LAST) qa = fma_e(d0, d0, qa);
+      }
+      if (real(i + 1)) {
+        sb += d1;
+        if (!LAST) qb = fma_e(d1, d1, qb);
+      }
+      if (LAST && ARGMAX) {  // slots in increasing element order: strict > keeps the lowest index
+        if (d0 > bestv) { bestv = d0; besto = i; }
+        if (d1 > bestv) { bestv = d1; besto = i + 1; }
+      }
+    }
+    if (FIRST) ptx::fence_proxy_async_smem();  // side writes -> visible to the TMA engine after the barrier
+  };
 
   // ---- T iterations; the last one (no variance; argmax) is peeled -----------
   double total = 0.0;
@@ -387,7 +537,6 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], PassToken<NTG, G>& tok,
       stats_row[t * 2 + 0] = mu;
       stats_row[t * 2 + 1] = s2;
     }
-    if (t == 0) PAM_TRACE(tr, 29);
     double inv_sigma;
     if (!poly_invsqrt) {
       inv_sigma = rsqrt(s2);  // ~1 ulp; identical in every CTA of the cluster
@@ -399,68 +548,44 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], PassToken<NTG, G>& tok,
         if (rs) st = rs;
       }
     }
-    if (t == 0) PAM_TRACE(tr, 30);
     const double kd = (st == PAM_OK) ? inv_sigma * c_inv : 0.0;
     const double bd = fma(-dm, kd, 1.0);
-    const Elem ke = (Elem)kd, be = (Elem)bd, kn = (Elem)(-knext);
+    const Elem ke = (Elem)kd, be = affine_coef<Elem>(bd, dm), kn = (Elem)(-knext);
     const int p = pcur;
-    if (t == 0) PAM_TRACE(tr, 27);
     w = cutmax_update<Elem, P>(w, ke, be, kn, p);
     const double kthis = knext;
-    tok.take();
+    const bool first = (t == 0) && h.pass0_on;
+    Elem sa = 0, sb = 0, qa = 0, qb = 0, bestv = -INFINITY;
+    int besto = 0;  // register slot of the best element (compile-time immediates)
     if (t + 1 < T) {
-      Elem sa = 0, sb = 0, qa = 0, qb = 0;
-#pragma unroll
-      for (int i = 0; i < E; i += 2) {
-        const Elem d0 = cutmax_update<Elem, P>(v[i], ke, be, kn, p);
-        const Elem d1 = cutmax_update<Elem, P>(v[i + 1], ke, be, kn, p);
-        v[i] = d0;
-        v[i + 1] = d1;
-        sa += d0;
-        sb += d1;
-        qa = fma_e(d0, d0, qa);
-        qb = fma_e(d1, d1, qb);
-      }
+      if (first)
+        pass(BoolC<true>(), BoolC<false>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
+      else
+        pass(BoolC<false>(), BoolC<false>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
       c_inv = rp.inv_c[t + 1];  // prefetch next iteration's constants
       knext = rp.kshift[t + 2];
       pcur = rp.p[t + 1];
       PAM_TRACE(tr, 5 + 2 * t);
-      tok.give();
-      const double2 r =
-          cluster_sum2<NTG>((double)sa + (double)sb, (double)qa + (double)qb, cb, xround, rank, C, g, gtid);
+      xch_push<NTG, kSum2>((double)sa + (double)sb, (double)qa + (double)qb, 0.0, 0LL, cb, xround, rank, C, gtid,
+                           [&]() { h.side(t); });
+      double bv = 0.0;
+      long long bi = 0;
+      const double2 r = xch_wait<kSum2>(bv, bi, cb, xround, C, gtid);
       PAM_TRACE(tr, 6 + 2 * t);
-      // deferred work (the next-row prefetch into the landing buffer): the
-      // previous row's Z bulk store drains at the HBM write rate and holds the
-      // buffer for several exchanges, so wait until the third exchange
-      if (t == 1 || (t == 0 && T == 2)) after_first_xchg();
       const double wd = (double)w;
-      guard(r.x - mphantom * wd, r.y - mphantom * wd * wd, wd, dm, s2);
+      guard(r.x - mph * wd, r.y - mph * wd * wd, wd, dm, s2);
       kcur = kthis;
     } else {
-      Elem sa = 0, sb = 0;
-      Elem bestv = -INFINITY;
-      int besto = 0;  // register slot of the best element (compile-time immediates)
-#pragma unroll
-      for (int i = 0; i < E; i += 2) {
-        const Elem d0 = cutmax_update<Elem, P>(v[i], ke, be, kn, p);
-        const Elem d1 = cutmax_update<Elem, P>(v[i + 1], ke, be, kn, p);
-        v[i] = d0;
-        v[i + 1] = d1;
-        sa += d0;
-        sb += d1;
-        if (ARGMAX) {  // slots in increasing element order: strict > keeps the lowest index
-          if (d0 > bestv) { bestv = d0; besto = i; }
-          if (d1 > bestv) { bestv = d1; besto = i + 1; }
-        }
-      }
+      if (first)
+        pass(BoolC<true>(), BoolC<true>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
+      else
+        pass(BoolC<false>(), BoolC<true>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
       double best = (double)bestv;
       long long besti = gbase + (long long)(((besto / VEC) * NTG + gtid) * VEC + (besto % VEC));
       PAM_TRACE(tr, 5 + 2 * t);
-      tok.give();
-      const double2 r = cluster_reduce<NTG, ARGMAX>((double)sa + (double)sb, 0.0, best, besti, cb, xround, rank, C,
-                                                    g, gtid);
+      const double ty = h.final_xch((double)sa + (double)sb, best, besti);
       PAM_TRACE(tr, 6 + 2 * t);
-      total = r.x - mphantom * (double)w;  // kshift[T] == 0: v holds Y^(T+1) itself
+      total = ty - mph * (double)w;  // kshift[T] == 0: v holds Y^(T+1) itself
       argmax_out = besti;
     }
   }
@@ -483,27 +608,26 @@ __device__ __forceinline__ int cutmax_core(Elem (&v)[E], PassToken<NTG, G>& tok,
 // Resident CTAs per SM the register budget should allow (launch-bounds hint).
 template <typename Elem, int NT, int E>
 constexpr int min_blocks_for() {
-  constexpr int regs = E * (int)sizeof(Elem) / 4 + 48;
+  constexpr int regs = E * (int)sizeof(Elem) / 4 + 72;
   constexpr int b = 65536 / (NT * regs);
   return b < 1 ? 1 : (b > 8 ? 8 : b);
 }
 
 // ---------------------------------------------------------------------------
-template <typename Elem, int NTG, int G, int E, int P>
-__global__ void __launch_bounds__(NTG* G, (min_blocks_for<Elem, NTG * G, E>())) cutmax_rows_kernel(const CutmaxArgs a) {
+template <typename Elem, int NTG, int E, int P>
+__global__ void __launch_bounds__(NTG, (min_blocks_for<Elem, NTG, E>())) cutmax_rows_kernel(const CutmaxArgs a) {
   using Tr = ElemTraits<Elem>;
   using V = typename Tr::V;
   constexpr int VEC = Tr::VEC;
   constexpr int NV = E / VEC;
   constexpr int NW = NTG / 32;
   static_assert(E % VEC == 0 && E % 2 == 0, "E must be a multiple of the vector width");
-  static_assert(NTG % 32 == 0 && NW <= 16 && (NW & (NW - 1)) == 0, "bad group size");
+  static_assert(NTG % 32 == 0 && NW >= 2 && NW <= 16 && (NW & (NW - 1)) == 0, "bad CTA size");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int g = (G == 1) ? 0 : (int)(threadIdx.x / NTG);
-  const int gtid = (G == 1) ? (int)threadIdx.x : (int)(threadIdx.x % NTG);
-  Elem* buf = reinterpret_cast<Elem*>(smem_raw + g * a.buf_bytes);
-  ControlBlock* cb = reinterpret_cast<ControlBlock*>(smem_raw + a.ctrl_offset) + g;
+  const int gtid = (int)threadIdx.x;
+  Elem* buf = reinterpret_cast<Elem*>(smem_raw);  // row buffer: NTG*E elements (TMA path)
+  ControlBlock* cb = reinterpret_cast<ControlBlock*>(smem_raw + a.ctrl_offset);
 
   const uint32_t rank = ptx::cluster_ctarank();
   const uint32_t C = ptx::cluster_nctarank();
@@ -514,14 +638,22 @@ __global__ void __launch_bounds__(NTG* G, (min_blocks_for<Elem, NTG * G, E>())) 
   const int64_t rem = n - base;
   const int len = rem <= 0 ? 0 : (rem < a.L ? (int)rem : a.L);
   const bool TMA = a.tma != 0;
-  const double mphantom = (double)((int64_t)C * NTG * E - n);  // phantom slots in the cluster
+  const bool dma = gtid == NTG - 32;  // lane 0 of the last warp issues every bulk copy
+  // phantom handling (see cutmax_iterate): fp64 subtracts mph * w from the
+  // cluster sums, fp32 predicates the accumulation on real(i)
+  const double mph = sizeof(Elem) == 8 ? (double)((int64_t)C * NTG * E - n) : 0.0;
+  auto real = [&](int i) { return sizeof(Elem) == 8 || ((i / VEC) * NTG + gtid) * VEC + (i % VEC) < len; };
   const RowParams& rp = a.rp;
   const int T = rp.T;
   const Elem* __restrict__ X = reinterpret_cast<const Elem*>(a.x);
   Elem* __restrict__ Z = reinterpret_cast<Elem*>(a.z);
 
   const uint32_t bar_load = ptx::smem_addr(&cb->mb_load);
-  const uint32_t load_bytes = (uint32_t)len * (uint32_t)sizeof(Elem);
+  const uint32_t slice_bytes = (uint32_t)len * (uint32_t)sizeof(Elem);
+  // bulk copies move the slice in 4 chunks so a row's load can chase the
+  // previous row's store through the buffer chunk by chunk
+  const uint32_t chunk = ((slice_bytes + 63u) / 64u) * 16u;
+  const int nch = chunk ? (int)((slice_bytes + chunk - 1) / chunk) : 0;
   uint64_t policy = 0;
   if (TMA) policy = ptx::policy_evict_first();
 
@@ -529,176 +661,602 @@ __global__ void __launch_bounds__(NTG* G, (min_blocks_for<Elem, NTG * G, E>())) 
     ptx::mbar_init(bar_load, 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[0]), 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[1]), 1);
+    ptx::mbar_init(ptx::smem_addr(&cb->mb_in), 1);
     ptx::fence_mbar_init();
   }
   __syncthreads();
   if (gtid == 0) {
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 32u);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 32u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_in), C * 16u);
   }
   ptx::cluster_sync();
 
-  auto issue_load = [&](int64_t row) {
-    // one elected thread: arm the load barrier and stream the slice in 32 KB pieces
-    ptx::mbar_arrive_expect_tx(bar_load, load_bytes);
+  // ---- DMA-thread helpers ----------------------------------------------------
+  auto load_chunk = [&](int64_t row, int i) {
     const unsigned char* src = reinterpret_cast<const unsigned char*>(X + row * a.ldx + base);
-    const uint32_t dst = ptx::smem_addr(buf);
-    for (uint32_t off = 0; off < load_bytes; off += 32768u) {
-      const uint32_t nb = (load_bytes - off) < 32768u ? (load_bytes - off) : 32768u;
-      ptx::bulk_g2s(dst + off, src + off, nb, bar_load, policy);
+    const uint32_t off = (uint32_t)i * chunk;
+    const uint32_t nb = (slice_bytes - off) < chunk ? (slice_bytes - off) : chunk;
+    ptx::bulk_g2s(ptx::smem_addr(buf) + off, src + off, nb, bar_load, policy);
+  };
+  auto store_all = [&](int64_t row) {  // buf -> Z(row), one bulk group per chunk
+    if (a.debug_flags & 1) return;
+    unsigned char* dst = reinterpret_cast<unsigned char*>(Z + row * a.ldz + base);
+    for (int i = 0; i < nch; ++i) {
+      const uint32_t off = (uint32_t)i * chunk;
+      const uint32_t nb = (slice_bytes - off) < chunk ? (slice_bytes - off) : chunk;
+      ptx::bulk_s2g(dst + off, ptx::smem_addr(buf) + off, nb, policy);
+      ptx::bulk_commit();
+    }
+  };
+  auto load_after_store = [&](int64_t row) {  // X(row) -> buf as the outstanding store frees each chunk
+    ptx::mbar_arrive_expect_tx(bar_load, slice_bytes);
+    const bool st_out = !(a.debug_flags & 1);
+    for (int i = 0; i < nch; ++i) {
+      if (st_out) ptx::bulk_wait_read_le(nch - 1 - i);
+      load_chunk(row, i);
     }
   };
 
-  const int64_t row0 = cid * G + g, rstride = ncl * G;
-  uint32_t xround = 0, load_par = 0;
-  // De-phase the row streams (dev knob, default off).
-  if (a.stagger > 0) {
-    const long long wait = a.stagger * (long long)(g * ncl + cid) / (long long)(G * ncl);
-    const long long t0 = clock64();
-    while (clock64() - t0 < wait) __nanosleep(256);
-  }
-
+  int64_t row = cid;
+  uint32_t xround = 0, load_par = 0, in_par = 0;
   Elem v[E];
-  // Register <- shared-memory slice copy (phantoms = k0).  Used for the first row.
-  auto lds_slice = [&](Elem k0) {
+
+  // ---- prologue: the cluster's first row -> registers -------------------------
+  if (TMA && row < a.B) {
+    if (dma) {
+      ptx::mbar_arrive_expect_tx(bar_load, slice_bytes);
+      for (int i = 0; i < nch; ++i) load_chunk(row, i);
+    }
+    ptx::mbar_wait_cta(bar_load, load_par);
+    load_par ^= 1u;
+    const Elem k0 = __ldg(X + row * a.ldx);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const int li0 = (k * NTG + gtid) * VEC;
       if (li0 + VEC <= len) {
-        const V t = *reinterpret_cast<const V*>(buf + li0);
-        *reinterpret_cast<V*>(&v[k * VEC]) = t;
+        *reinterpret_cast<V*>(&v[k * VEC]) = *reinterpret_cast<const V*>(buf + li0);
       } else {
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) v[k * VEC + j] = (li0 + j < len) ? buf[li0 + j] : k0;
+        for (int j = 0; j < VEC; ++j) v[k * VEC + j] = (li0 + j < len) ? buf[li0 + j] : k0;  // phantoms = K0
       }
     }
-  };
-
-  // TMA pipeline per group (landing buffer `buf`):
-  //   row r computes from registers while buf receives X(r+1);
-  //   at the end of row r each thread swaps Z(r) into buf and X(r+1) into its
-  //   registers, and one thread streams buf -> Z(r) with a bulk TMA store;
-  //   once that store has read buf (checked after the next row's first
-  //   exchange) the load of X(r+2) is issued into buf.
-  if (TMA && gtid == 0 && row0 < a.B) issue_load(row0);
-  if (TMA && row0 < a.B) {
-    ptx::mbar_wait_cta(bar_load, load_par);
-    load_par ^= 1u;
-    lds_slice(__ldg(X + row0 * a.ldx));
-    group_sync<NTG>(g);  // buf free
+    __syncthreads();  // buf free
   }
-  bool need_issue = TMA;  // deferred prefetch of the row after next
 
-  // Row slots: both groups of a CTA walk the same number of slots so their pass
-  // tokens stay balanced (a group without a row in its last slot idles).
-  const int64_t first0 = cid * G;
-  const int64_t K = (a.B > first0) ? (a.B - first0 + rstride - 1) / rstride : 0;
-  PassToken<NTG, G> tok(g, K * (int64_t)(T + 1));
-  for (int64_t k = 0; k < K; ++k) {
-    const int64_t row = row0 + k * rstride;
-    if (row >= a.B) {  // idle slot: keep the token moving
-      for (int ph = 0; ph <= T; ++ph) {
-        tok.take();
-        tok.give();
-      }
-      continue;
-    }
-    const int64_t next = row + rstride;
-    const bool has_next = next < a.B;
-    const int64_t lrow = k;
-    // trace: group g uses rows [g*kTraceRows/G, (g+1)*kTraceRows/G) of its CTA's trace block
-    long long* tr = (a.trace && lrow < kTraceRows / G)
-                        ? a.trace + ((int64_t)blockIdx.x * kTraceRows + g * (kTraceRows / G) + lrow) * kTraceEvents
-                        : nullptr;
-    PAM_TRACE(tr, 0);
-    const Elem* xrow = X + row * a.ldx;
-    const Elem k0e = __ldg(xrow);  // shift for the input pass (same in every CTA)
-    const double K0 = (double)k0e;
-    const Elem k0next = has_next ? __ldg(X + next * a.ldx) : Elem(0);
-    tok.take();  // input pass (shift + moments) needs the fp64 pipe
-
-    if (!TMA) {  // unaligned rows: direct loads, no staging
-      const Elem* src = xrow + base;
+  if constexpr (P == 3) {
+    // ===== p = 3 every iteration: analytic normaliser =======================
+    // sum_i (1 + k d_i)^3 = n + 3k sum d + 3k^2 sum d^2 + k^3 sum d^3 with
+    // d = y - mu of the iterate feeding the last iteration, so inv(sum Y) is
+    // known BEFORE the last pass.  The last pass then writes Z = Y*inv directly
+    // into the row buffer while pulling X(next) - K0(next) into registers and
+    // summing its moments; ONE exchange closes the row (argmax + next row's
+    // input sums) and the Z store streams out right behind it.  The third
+    // power sum rides on the exchange of pass T-2 (or the input for T = 1).
+    // A non-finite analytic total (third powers overflowing) falls back to an
+    // explicit sum of Y (extra pass + exchange).
+    constexpr double kGuard = sizeof(Elem) == 8 ? 16.0 : 2.0;
+    const double nd = (double)n;
+    const double inv_n = a.inv_n;
+    const bool normalize = !(rp.flags & PAM_F_NO_NORMALIZE);
+    const bool poly_invsqrt = rp.invsqrt_mode == PAM_MODE_POLY;
+    const double eps_var = rp.eps_var;
+    bool in_ready = false;  // registers hold the K0-shifted row, (S_in, Q_in, R_in) its cluster sums
+    double S_in = 0.0, Q_in = 0.0, R_in = 0.0;
+#ifdef PAM_TRACE_BUILD
+    int64_t lrow = 0;
+#endif
+    for (; row < a.B; row += ncl) {
+      const int64_t next = row + ncl;
+      const bool has_next = next < a.B;
+      const bool merged = TMA && has_next;  // the closing exchange carries the next row's input sums
+#ifdef PAM_TRACE_BUILD
+      long long* tr = (a.trace && lrow < kTraceRows)
+                          ? a.trace + ((int64_t)blockIdx.x * kTraceRows + lrow) * kTraceEvents
+                          : nullptr;
+#else
+      long long* tr = nullptr;
+#endif
+      PAM_TRACE(tr, 0);
+      const Elem* xrow = X + row * a.ldx;
+      const Elem k0e = __ldg(xrow);  // shift for the input (same in every CTA)
+      const double K0 = (double)k0e;
+      const Elem k0next = has_next ? __ldg(X + next * a.ldx) : Elem(0);
+      if (!in_ready) {
+        if (!TMA) {  // unaligned rows: direct loads, no staging
+          const Elem* src = xrow + base;
 #pragma unroll
-      for (int kk = 0; kk < NV; ++kk) {
-        const int li0 = (kk * NTG + gtid) * VEC;
+          for (int kk = 0; kk < NV; ++kk) {
+            const int li0 = (kk * NTG + gtid) * VEC;
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) v[kk * VEC + j] = (li0 + j < len) ? __ldcs(src + li0 + j) : k0e;
+            for (int j = 0; j < VEC; ++j) v[kk * VEC + j] = (li0 + j < len) ? __ldcs(src + li0 + j) : k0e;
+          }
+        }
+        const double3 part = input_pass3<Elem, E>(v, K0);
+        const double3 r = cluster_sum3<NTG>(part.x, part.y, part.z, cb, xround, rank, C, gtid);
+        S_in = r.x;
+        Q_in = r.y;
+        R_in = r.z;
       }
-    }
-    PAM_TRACE(tr, 2);
+      PAM_TRACE(tr, 2);
 
-    // deferred: once the previous Z store has read buf, prefetch X(next) into it
-    auto prefetch_next = [&]() {
-      if (need_issue && gtid == 0) {
-        ptx::bulk_wait_read_all();
-        if (has_next) issue_load(next);
-      }
-    };
+      // DMA thread: X(next) -> buffer, chunk by chunk behind the previous row's Z store
+      int issued = 0;
+      bool armed = false;
+      auto issue_upto = [&](int upto) {
+        if (!merged) return;
+        if (!armed) {
+          ptx::mbar_arrive_expect_tx(bar_load, slice_bytes);
+          armed = true;
+        }
+        const bool st_out = !(a.debug_flags & 1);
+        for (; issued < upto; ++issued) {
+          if (st_out) ptx::bulk_wait_read_le(nch - 1 - issued);
+          load_chunk(next, issued);
+        }
+      };
+      auto side = [&](int e) {
+        if (e == 0) issue_upto(nch / 2);
+        if (e == 1) issue_upto(nch);
+        PAM_TRACE_DMA(tr, 25 + (e < 2 ? e : 1));
+      };
 
-    // ---- input statistics + T CutMax iterations + normaliser + argmax ------------
-    double rnorm = 1.0;
-    long long amax = -1;
-    const int st = cutmax_core<Elem, NTG, G, E, P, true>(
-        v, tok, K0, mphantom, rp, a.inv_n, cb, xround, rank, C, g, gtid, base,
-        (rank == 0 && gtid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr, rnorm, amax, tr, prefetch_next);
-    PAM_TRACE(tr, 20);
-    if (rank == 0 && gtid == 0) {
-      if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)amax : -1;
-      if (a.status) a.status[row] = st;
-    }
-
-    // ---- Z = Y * inv(sum Y) ------------------------------------------------------
-    const Elem re = (Elem)rnorm;
-    Elem* zrow = Z + row * a.ldz + base;
-    if (TMA) {
-      // swap: Z(row) -> buf, X(next) -> registers; then bulk-store buf -> Z(row)
-      if (has_next) {
-        ptx::mbar_wait_cta(bar_load, load_par);
-        load_par ^= 1u;
-      }
+      int st = PAM_OK;
+      double dm = 0.0, s2 = 0.0, m3 = 0.0, e1 = 0.0;
+      // moments of the current iterate from its shifted cluster sums (+ the
+      // exact second pass when the one-pass form cancelled, see header)
+      auto moments = [&](double S, double Q, double R, double w, bool need3) {
+        dm = S * inv_n;
+        const double qn = Q * inv_n;
+        s2 = fma(-dm, dm, qn);
+        if (need3) {
+          e1 = fma(-nd, dm, S);
+          m3 = fma(dm, fma(2.0 * dm, dm, -3.0 * qn), R * inv_n);
+        }
+        if (st == PAM_OK && isfinite(Q) && qn > kGuard * s2) {
+          const Elem dme = (Elem)dm;
+          Elem q2a = 0, q2b = 0, r3a = 0, r3b = 0;
 #pragma unroll
-      for (int kk = 0; kk < NV; ++kk) {
-        const int li0 = (kk * NTG + gtid) * VEC;
-        Elem o[VEC];
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) o[j] = v[kk * VEC + j] * re;
-        if (li0 + VEC <= len) {
-          const V xn = *reinterpret_cast<const V*>(buf + li0);
-          *reinterpret_cast<V*>(buf + li0) = *reinterpret_cast<V*>(o);
-          *reinterpret_cast<V*>(&v[kk * VEC]) = xn;
+          for (int i = 0; i < E; i += 2) {
+            const Elem d0 = v[i] - dme, d1 = v[i + 1] - dme;
+            const Elem f0 = d0 * d0, f1 = d1 * d1;
+            if (real(i)) {
+              q2a += f0;
+              r3a = fma_e(f0, d0, r3a);
+            }
+            if (real(i + 1)) {
+              q2b += f1;
+              r3b = fma_e(f1, d1, r3b);
+            }
+          }
+          const double2 r2 =
+              cluster_sum2<NTG>((double)q2a + (double)q2b, (double)r3a + (double)r3b, cb, xround, rank, C, gtid);
+          const double dw = (double)((Elem)w - dme);
+          s2 = (r2.x - mph * dw * dw) * inv_n;
+          if (need3) m3 = (r2.y - mph * dw * dw * dw) * inv_n;
+        }
+      };
+      if (!isfinite(S_in) || !isfinite(Q_in)) st = PAM_ERR_NON_FINITE;
+      moments(S_in, Q_in, R_in, 0.0, T == 1);
+      PAM_TRACE(tr, 4);
+
+      double* stats_row = (rank == 0 && gtid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr;
+      double kcur = K0, c_inv = rp.inv_c[0], knext = rp.kshift[1];
+      double kd = 0.0, bd = 1.0;
+      // scalar chain of iteration t: status, k = inv_sigma / c, b = 1 - dm k
+      auto chain = [&](int t) {
+        const double mu = kcur + dm;
+        const bool bad_range = !isfinite(mu) || !isfinite(s2);
+        st = (st != PAM_OK) ? st : (bad_range ? PAM_ERR_RANGE : (s2 < eps_var ? PAM_ERR_DEGENERATE_INPUT : PAM_OK));
+        if (stats_row) {
+          stats_row[t * 2 + 0] = mu;
+          stats_row[t * 2 + 1] = s2;
+        }
+        double inv_sigma;
+        if (!poly_invsqrt) {
+          inv_sigma = rsqrt(s2);  // ~1 ulp; identical in every CTA of the cluster
         } else {
+          const pam_approx_config& ac = rp.invsqrt[t];
+          inv_sigma = 0.0;
+          if (st == PAM_OK) {
+            const int rs = invsqrt_rescaled(s2, ac.iterations, ac.rescale, ac.scale_log2, ac.lo, ac.hi, &inv_sigma);
+            if (rs) st = rs;
+          }
+        }
+        kd = (st == PAM_OK) ? inv_sigma * c_inv : 0.0;
+        bd = fma(-dm, kd, 1.0);
+      };
+
+      Elem w = 0;  // phantom value (shifted representation)
+      // pass t < T-1: update + shifted moments (+ third power sum on pass T-2)
+      auto pass = [&](auto r_c, Elem ke, Elem be, Elem kn, double3& out) {
+        constexpr bool R3 = decltype(r_c)::value;
+        Elem sa = 0, sb = 0, qa = 0, qb = 0, ra = 0, rb = 0;
 #pragma unroll
-          for (int j = 0; j < VEC; ++j) {
-            const Elem xn = (li0 + j < len) ? buf[li0 + j] : k0next;
-            if (li0 + j < len) buf[li0 + j] = o[j];
-            v[kk * VEC + j] = xn;
+        for (int i = 0; i < E; i += 2) {
+          const Elem d0 = cutmax_update<Elem, 3>(v[i], ke, be, kn, 3);
+          const Elem d1 = cutmax_update<Elem, 3>(v[i + 1], ke, be, kn, 3);
+          v[i] = d0;
+          v[i + 1] = d1;
+          if (R3) {
+            const Elem f0 = d0 * d0, f1 = d1 * d1;
+            if (real(i)) {
+              sa += d0;
+              qa += f0;
+              ra = fma_e(f0, d0, ra);
+            }
+            if (real(i + 1)) {
+              sb += d1;
+              qb += f1;
+              rb = fma_e(f1, d1, rb);
+            }
+          } else {
+            if (real(i)) {
+              sa += d0;
+              qa = fma_e(d0, d0, qa);
+            }
+            if (real(i + 1)) {
+              sb += d1;
+              qb = fma_e(d1, d1, qb);
+            }
+          }
+        }
+        out = make_double3((double)sa + (double)sb, (double)qa + (double)qb, (double)ra + (double)rb);
+      };
+      for (int t = 0; t + 1 < T; ++t) {
+        chain(t);
+        const Elem ke = (Elem)kd, be = affine_coef<Elem>(bd, dm), kn = (Elem)(-knext);
+        w = cutmax_update<Elem, 3>(w, ke, be, kn, 3);
+        const double kthis = knext;
+        const bool need3 = (t + 2 == T);
+        double3 part;
+        if (need3)
+          pass(BoolC<true>(), ke, be, kn, part);
+        else
+          pass(BoolC<false>(), ke, be, kn, part);
+        c_inv = rp.inv_c[t + 1];  // prefetch next iteration's constants
+        knext = rp.kshift[t + 2];
+        PAM_TRACE(tr, 5 + 2 * t);
+        double r3 = 0.0;
+        long long ci = 0;
+        double2 r;
+        if (need3) {
+          xch_push<NTG, kSum3>(part.x, part.y, part.z, 0LL, cb, xround, rank, C, gtid, [&]() { side(t); });
+          r = xch_wait<kSum3>(r3, ci, cb, xround, C, gtid);
+        } else {
+          xch_push<NTG, kSum2>(part.x, part.y, 0.0, 0LL, cb, xround, rank, C, gtid, [&]() { side(t); });
+          r = xch_wait<kSum2>(r3, ci, cb, xround, C, gtid);
+        }
+        PAM_TRACE(tr, 6 + 2 * t);
+        const double wd = (double)w;
+        moments(r.x - mph * wd, r.y - mph * wd * wd, r3 - mph * wd * wd * wd, wd, need3);
+        kcur = kthis;
+      }
+
+      // ---- last iteration: normaliser first, then the fused pass ---------------
+      chain(T - 1);
+      const Elem ke = (Elem)kd, be = affine_coef<Elem>(bd, dm), kz = (Elem)0;  // kshift[T] = 0
+      double rnorm = 1.0;
+      {
+        double total = nd + kd * (3.0 * e1 + kd * (3.0 * nd * s2 + kd * nd * m3));
+        if (st == PAM_OK && !isfinite(total)) {  // explicit sum (rare)
+          Elem ta = 0, tb = 0;
+#pragma unroll
+          for (int i = 0; i < E; i += 2) {
+            const Elem y0 = cutmax_update<Elem, 3>(v[i], ke, be, kz, 3);
+            const Elem y1 = cutmax_update<Elem, 3>(v[i + 1], ke, be, kz, 3);
+            if (real(i)) ta += y0;
+            if (real(i + 1)) tb += y1;
+          }
+          total = cluster_sum2<NTG>((double)ta + (double)tb, 0.0, cb, xround, rank, C, gtid).x -
+                  mph * (double)cutmax_update<Elem, 3>(w, ke, be, kz, 3);
+        }
+        if (st == PAM_OK && !isfinite(total)) st = PAM_ERR_RANGE;
+        if (st == PAM_OK && normalize) {
+          if (!(total > 0.0)) {
+            st = PAM_ERR_RANGE;  // Z must be a distribution (pin A7)
+          } else if (rp.inv_mode == PAM_MODE_POLY) {
+            const pam_approx_config& ac = rp.inv;
+            const int rs = inv_rescaled(total, ac.iterations, ac.rescale, ac.scale_log2, ac.lo, ac.hi, &rnorm);
+            if (rs) st = rs;
+          } else {
+            rnorm = 1.0 / total;
           }
         }
       }
-      ptx::fence_proxy_async_smem();  // make the Z writes visible to the TMA engine
-      group_sync<NTG>(g);
-      if (gtid == 0 && !(a.debug_flags & 1)) {
-        const uint32_t zbytes = load_bytes;
-        const unsigned char* dstb = reinterpret_cast<const unsigned char*>(zrow);
-        for (uint32_t off = 0; off < zbytes; off += 32768u) {
-          const uint32_t nb = (zbytes - off) < 32768u ? (zbytes - off) : 32768u;
-          ptx::bulk_s2g((void*)(dstb + off), ptx::smem_addr(buf) + off, nb, policy);
+      const Elem re = (Elem)rnorm;
+      PAM_TRACE(tr, 22);
+      if (merged) {
+        if (dma) issue_upto(nch);  // small T: whatever the hooks did not issue yet
+        ptx::mbar_wait_cta(bar_load, load_par);  // X(next) has landed
+        load_par ^= 1u;
+      } else if (TMA) {
+        if (dma) ptx::bulk_wait_read_all();  // the previous Z store has read the buffer
+        __syncthreads();
+      }
+      PAM_TRACE(tr, 23);
+
+      // fused last pass: Y = z^3 (argmax), Z = Y * inv(sum Y) -> buffer / HBM,
+      // and (merged) X(next) - K0(next) -> registers with its moments
+      Elem bestv = -INFINITY;
+      int besto = 0;  // register slot of the best element (compile-time immediates)
+      double3 nxt = make_double3(0.0, 0.0, 0.0);
+      Elem* zrow = Z + row * a.ldz + base;
+      auto last = [&](auto mode_c, auto r_c) {
+        constexpr int MODE = decltype(mode_c)::value;  // 0: swap (merged), 1: Z -> buffer, 2: Z -> HBM
+        constexpr bool R3 = decltype(r_c)::value;
+        Elem sa = 0, sb = 0, qa = 0, qb = 0, ra = 0, rb = 0;
+#pragma unroll
+        for (int kk = 0; kk < NV; ++kk) {
+          const int li0 = (kk * NTG + gtid) * VEC;
+          Elem o[VEC];
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) {
+            const Elem y = cutmax_update<Elem, 3>(v[kk * VEC + j], ke, be, kz, 3);
+            if (y > bestv) {  // slots in increasing element order: strict > keeps the lowest index
+              bestv = y;
+              besto = kk * VEC + j;
+            }
+            o[j] = y * re;
+          }
+          if (MODE == 2) {
+            if (!(a.debug_flags & 1)) {
+#pragma unroll
+              for (int j = 0; j < VEC; ++j)
+                if (li0 + j < len) __stcs(zrow + li0 + j, o[j]);
+            }
+            continue;
+          }
+          if (li0 + VEC <= len) {
+            V xn;
+            if (MODE == 0) xn = *reinterpret_cast<const V*>(buf + li0);
+            *reinterpret_cast<V*>(buf + li0) = *reinterpret_cast<const V*>(o);
+            if (MODE == 0) {
+              const Elem* xe = reinterpret_cast<const Elem*>(&xn);
+#pragma unroll
+              for (int j = 0; j < VEC; ++j) v[kk * VEC + j] = xe[j] - k0next;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) {
+              const bool in = li0 + j < len;
+              Elem xv = k0next;  // phantoms: K0(next) -> 0
+              if (MODE == 0 && in) xv = buf[li0 + j];
+              if (in) buf[li0 + j] = o[j];
+              if (MODE == 0) v[kk * VEC + j] = xv - k0next;
+            }
+          }
+          if (MODE == 0) {
+#pragma unroll
+            for (int j = 0; j < VEC; j += 2) {
+              const Elem d0 = v[kk * VEC + j], d1 = v[kk * VEC + j + 1];
+              sa += d0;
+              sb += d1;
+              if (R3) {
+                const Elem f0 = d0 * d0, f1 = d1 * d1;
+                qa += f0;
+                qb += f1;
+                ra = fma_e(f0, d0, ra);
+                rb = fma_e(f1, d1, rb);
+              } else {
+                qa = fma_e(d0, d0, qa);
+                qb = fma_e(d1, d1, qb);
+              }
+            }
+          }
         }
-        ptx::bulk_commit();
+        nxt = make_double3((double)sa + (double)sb, (double)qa + (double)qb, (double)ra + (double)rb);
+      };
+      if (merged) {
+        if (T == 1)
+          last(IntC<0>(), BoolC<true>());
+        else
+          last(IntC<0>(), BoolC<false>());
+      } else if (TMA) {
+        last(IntC<1>(), BoolC<false>());
+      } else {
+        last(IntC<2>(), BoolC<false>());
       }
-    } else if (!(a.debug_flags & 1)) {
-#pragma unroll
-      for (int kk = 0; kk < NV; ++kk) {
-        const int li0 = (kk * NTG + gtid) * VEC;
-#pragma unroll
-        for (int j = 0; j < VEC; ++j)
-          if (li0 + j < len) __stcs(zrow + li0 + j, v[kk * VEC + j] * re);
+      if (TMA) ptx::fence_proxy_async_smem();  // Z writes -> visible to the TMA engine after the barrier
+      PAM_TRACE(tr, 24);
+      double best = (double)bestv;
+      long long besti = base + (long long)(((besto / VEC) * NTG + gtid) * VEC + (besto % VEC));
+      const int64_t zr = row;
+      xch_push<NTG, kArgmax>(nxt.x, nxt.y, best, besti, cb, xround, rank, C, gtid, [&]() {
+        if (TMA) store_all(zr);
+      });
+      const double2 rn = xch_wait<kArgmax>(best, besti, cb, xround, C, gtid);
+      PAM_TRACE(tr, 6 + 2 * (T - 1));
+      if (merged) {
+        S_in = rn.x;
+        Q_in = rn.y;
+        if (T == 1) R_in = cluster_sum2<NTG>(nxt.z, 0.0, cb, xround, rank, C, gtid).x;
       }
+      in_ready = merged;
+      if (rank == 0 && gtid == 0) {
+        if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)besti : -1;
+        if (a.status) a.status[row] = st;
+      }
+      PAM_TRACE(tr, 21);
+#ifdef PAM_TRACE_BUILD
+      ++lrow;
+#endif
     }
-    PAM_TRACE(tr, 21);
+  } else {
+    // ===== generic p: one-pass-late normalisation (see header) ==============
+    bool in_ready = false;  // registers hold the K0-shifted row and (S_in, Q_in) its cluster sums
+    double S_in = 0.0, Q_in = 0.0;
+    bool zpend = false;  // buf holds the previous row's unnormalised Y: scale in pass 0, then store
+    Elem rn_prev = 1;
+    int64_t zrow_prev = 0;
+    const int pf_ex = T >= 3 ? 1 : 0;  // exchange whose DMA hook issues the next row's load
+  #ifdef PAM_TRACE_BUILD
+    int64_t lrow = 0;
+  #endif
+    for (; row < a.B; row += ncl) {
+      const int64_t next = row + ncl;
+      const bool has_next = next < a.B;
+      const bool merged = TMA && has_next;  // row-boundary exchange carries the next row's input sums
+  #ifdef PAM_TRACE_BUILD
+      long long* tr =
+          (a.trace && lrow < kTraceRows) ? a.trace + ((int64_t)blockIdx.x * kTraceRows + lrow) * kTraceEvents : nullptr;
+  #else
+      long long* tr = nullptr;
+  #endif
+      PAM_TRACE(tr, 0);
+      const Elem* xrow = X + row * a.ldx;
+      const Elem k0e = __ldg(xrow);  // shift for the input (same in every CTA)
+      const double K0 = (double)k0e;
+      const Elem k0next = has_next ? __ldg(X + next * a.ldx) : Elem(0);
+
+      if (!in_ready) {
+        if (!TMA) {  // unaligned rows: direct loads, no staging
+          const Elem* src = xrow + base;
+  #pragma unroll
+          for (int kk = 0; kk < NV; ++kk) {
+            const int li0 = (kk * NTG + gtid) * VEC;
+  #pragma unroll
+            for (int j = 0; j < VEC; ++j) v[kk * VEC + j] = (li0 + j < len) ? __ldcs(src + li0 + j) : k0e;
+          }
+        }
+        const double2 part = input_pass<Elem, E>(v, K0);
+        const double2 r = cluster_sum2<NTG>(part.x, part.y, cb, xround, rank, C, gtid);
+        S_in = r.x;
+        Q_in = r.y;
+      }
+      PAM_TRACE(tr, 2);
+
+      const bool scale_now = zpend;
+      const Elem rsc = rn_prev;
+      const int64_t zrow_p = zrow_prev;
+      auto pass0 = [&](int kk) {  // Z(prev) = Y(prev) * inv(sum Y(prev)), in the row buffer
+        V* p = reinterpret_cast<V*>(buf) + kk * NTG + gtid;
+        V t = *p;
+        Elem* te = reinterpret_cast<Elem*>(&t);
+  #pragma unroll
+        for (int j = 0; j < VEC; ++j) te[j] *= rsc;
+        *p = t;
+      };
+      auto side = [&](int e) {  // DMA thread, inside exchange e
+        if (!TMA) return;
+        if (e == 0 && scale_now) {
+          store_all(zrow_p);
+          PAM_TRACE_DMA(tr, 25);
+        }
+        if (e == pf_ex && has_next) {
+          PAM_TRACE_DMA(tr, 26);
+          load_after_store(next);
+          PAM_TRACE_DMA(tr, 27);
+        }
+      };
+      auto final_xch = [&](double sy, double& best, long long& besti) -> double {
+        xch_push<NTG, kArgmax>(sy, 0.0, best, besti, cb, xround, rank, C, gtid, [&]() { side(T - 1); });
+        if (merged) {
+          PAM_TRACE(tr, 22);
+          ptx::mbar_wait_cta(bar_load, load_par);  // X(next) has landed
+          load_par ^= 1u;
+          PAM_TRACE(tr, 23);
+          // swap: Y -> buf, X(next) - K0(next) -> registers (+ its moments)
+          Elem sa = 0, sb = 0, qa = 0, qb = 0;
+  #pragma unroll
+          for (int kk = 0; kk < NV; ++kk) {
+            const int li0 = (kk * NTG + gtid) * VEC;
+            if (li0 + VEC <= len) {
+              const V xn = *reinterpret_cast<const V*>(buf + li0);
+              *reinterpret_cast<V*>(buf + li0) = *reinterpret_cast<const V*>(&v[kk * VEC]);
+              const Elem* xe = reinterpret_cast<const Elem*>(&xn);
+  #pragma unroll
+              for (int j = 0; j < VEC; ++j) v[kk * VEC + j] = xe[j] - k0next;
+            } else {
+  #pragma unroll
+              for (int j = 0; j < VEC; ++j) {
+                const bool in = li0 + j < len;
+                const Elem xv = in ? buf[li0 + j] : k0next;  // phantoms: K0(next) -> 0
+                if (in) buf[li0 + j] = v[kk * VEC + j];
+                v[kk * VEC + j] = xv - k0next;
+              }
+            }
+  #pragma unroll
+            for (int j = 0; j < VEC; j += 2) {
+              const Elem d0 = v[kk * VEC + j], d1 = v[kk * VEC + j + 1];
+              sa += d0;
+              sb += d1;
+              qa = fma_e(d0, d0, qa);
+              qb = fma_e(d1, d1, qb);
+            }
+          }
+          xin_push<NTG>((double)sa + (double)sb, (double)qa + (double)qb, cb, rank, C, gtid);
+          PAM_TRACE(tr, 24);
+        }
+        double2 r = xch_wait<kArgmax>(best, besti, cb, xround, C, gtid);
+        if (merged) {
+          const double2 in = xin_wait(cb, in_par, C, gtid);
+          S_in = in.x;
+          Q_in = in.y;
+        }
+        return r.x;
+      };
+      auto hooks = make_hooks(scale_now, pass0, side, final_xch);
+
+      double rnorm = 1.0;
+      long long amax = -1;
+      const int st = cutmax_iterate<Elem, NTG, E, P, true>(
+          v, S_in, Q_in, K0, len, mph, rp, a.inv_n, cb, xround, rank, C, gtid, base,
+          (rank == 0 && gtid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr, rnorm, amax, hooks, tr);
+      PAM_TRACE(tr, 20);
+      if (rank == 0 && gtid == 0) {
+        if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)amax : -1;
+        if (a.status) a.status[row] = st;
+      }
+
+      const Elem re = (Elem)rnorm;
+      if (merged) {
+        zpend = true;  // Z(row) = buf * re, written during the next row's pass 0
+        rn_prev = re;
+        zrow_prev = row;
+        in_ready = true;
+      } else {
+        zpend = false;
+        in_ready = false;
+        if (TMA) {
+          // last row of this cluster: Z from registers through the buffer
+          if (dma) ptx::bulk_wait_read_all();  // the previous Z store has read buf
+          __syncthreads();
+  #pragma unroll
+          for (int kk = 0; kk < NV; ++kk) {
+            const int li0 = (kk * NTG + gtid) * VEC;
+            Elem o[VEC];
+  #pragma unroll
+            for (int j = 0; j < VEC; ++j) o[j] = v[kk * VEC + j] * re;
+            if (li0 + VEC <= len) {
+              *reinterpret_cast<V*>(buf + li0) = *reinterpret_cast<V*>(o);
+            } else {
+  #pragma unroll
+              for (int j = 0; j < VEC; ++j)
+                if (li0 + j < len) buf[li0 + j] = o[j];
+            }
+          }
+          ptx::fence_proxy_async_smem();  // make the Z writes visible to the TMA engine
+          __syncthreads();
+          if (dma) store_all(row);
+        } else if (!(a.debug_flags & 1)) {
+          Elem* zrow = Z + row * a.ldz + base;
+  #pragma unroll
+          for (int kk = 0; kk < NV; ++kk) {
+            const int li0 = (kk * NTG + gtid) * VEC;
+  #pragma unroll
+            for (int j = 0; j < VEC; ++j)
+              if (li0 + j < len) __stcs(zrow + li0 + j, v[kk * VEC + j] * re);
+          }
+        }
+      }
+      PAM_TRACE(tr, 21);
+  #ifdef PAM_TRACE_BUILD
+      ++lrow;
+  #endif
+    }
   }
-  if (TMA && gtid == 0) ptx::bulk_wait_all();  // Z stores complete before the CTA retires
+  if (TMA && dma) ptx::bulk_wait_all();  // Z stores complete before the CTA retires
   ptx::cluster_sync();  // no CTA leaves while a peer may still push into its shared memory
 }
 

@@ -1,34 +1,25 @@
-// cutmax_variants.cu — instantiations of cutmax_rows_kernel<Elem, NT, E, P, TMA>.
-// Per-CTA capacity NT*E elements; registers per thread ~ E*sizeof(Elem)/4 + ~30.
+// cutmax_variants.cu — instantiations of cutmax_rows_kernel<Elem, NTG, E, P>.
+// Per-CTA capacity NTG*E elements; registers per thread ~ E*sizeof(Elem)/4 + ~50.
 #include "cutmax_kernel.cuh"
 #include "pam_variants.h"
 
 namespace pam {
 
-#define PAM_CUTMAX_VARIANT(ELEM, NTG, G, E)                                    \
-  {                                                                           \
-    (int)sizeof(ELEM), NTG, G, E, {                                           \
-      (const void*)cutmax_rows_kernel<ELEM, NTG, G, E, 0>,                    \
-          (const void*)cutmax_rows_kernel<ELEM, NTG, G, E, 3>                 \
-    }                                                                         \
+#define PAM_CUTMAX_VARIANT(ELEM, NTG, E)                                                                 \
+  {                                                                                                    \
+    (int)sizeof(ELEM), NTG, E, {                                                                       \
+      (const void*)cutmax_rows_kernel<ELEM, NTG, E, 0>, (const void*)cutmax_rows_kernel<ELEM, NTG, E, 3> \
+    }                                                                                                  \
   }
 
-// Per-group capacity NTG*E elements; registers per thread ~ E*sizeof(Elem)/4 + ~40.
 const Variant kCutmaxVariants[] = {
-    PAM_CUTMAX_VARIANT(double, 64, 1, 2),   PAM_CUTMAX_VARIANT(double, 128, 1, 4),
-    PAM_CUTMAX_VARIANT(double, 128, 1, 8),  PAM_CUTMAX_VARIANT(double, 256, 1, 8),
-    PAM_CUTMAX_VARIANT(double, 256, 1, 16), PAM_CUTMAX_VARIANT(double, 512, 1, 16),
-    PAM_CUTMAX_VARIANT(double, 256, 1, 38), PAM_CUTMAX_VARIANT(double, 512, 1, 24),
-    PAM_CUTMAX_VARIANT(double, 512, 1, 38),
-    PAM_CUTMAX_VARIANT(double, 128, 2, 8),  PAM_CUTMAX_VARIANT(double, 256, 2, 16),
-    PAM_CUTMAX_VARIANT(double, 256, 2, 24), PAM_CUTMAX_VARIANT(double, 256, 2, 38),
-    PAM_CUTMAX_VARIANT(float, 64, 1, 4),    PAM_CUTMAX_VARIANT(float, 128, 1, 8),
-    PAM_CUTMAX_VARIANT(float, 256, 1, 8),   PAM_CUTMAX_VARIANT(float, 256, 1, 16),
-    PAM_CUTMAX_VARIANT(float, 512, 1, 16),  PAM_CUTMAX_VARIANT(float, 256, 1, 40),
-    PAM_CUTMAX_VARIANT(float, 512, 1, 24),  PAM_CUTMAX_VARIANT(float, 512, 1, 40),
-    PAM_CUTMAX_VARIANT(float, 256, 1, 76),
-    PAM_CUTMAX_VARIANT(float, 256, 2, 16),  PAM_CUTMAX_VARIANT(float, 256, 2, 40),
-    PAM_CUTMAX_VARIANT(float, 256, 2, 76),
+    PAM_CUTMAX_VARIANT(double, 64, 2),   PAM_CUTMAX_VARIANT(double, 128, 4),  PAM_CUTMAX_VARIANT(double, 128, 8),
+    PAM_CUTMAX_VARIANT(double, 256, 8),  PAM_CUTMAX_VARIANT(double, 256, 16), PAM_CUTMAX_VARIANT(double, 512, 16),
+    PAM_CUTMAX_VARIANT(double, 256, 38), PAM_CUTMAX_VARIANT(double, 512, 24), PAM_CUTMAX_VARIANT(double, 512, 30),
+    PAM_CUTMAX_VARIANT(double, 512, 34), PAM_CUTMAX_VARIANT(double, 512, 38),
+    PAM_CUTMAX_VARIANT(float, 64, 4),    PAM_CUTMAX_VARIANT(float, 128, 8),   PAM_CUTMAX_VARIANT(float, 256, 8),
+    PAM_CUTMAX_VARIANT(float, 256, 16),  PAM_CUTMAX_VARIANT(float, 512, 16),  PAM_CUTMAX_VARIANT(float, 256, 40),
+    PAM_CUTMAX_VARIANT(float, 512, 24),  PAM_CUTMAX_VARIANT(float, 512, 40),  PAM_CUTMAX_VARIANT(float, 256, 76),
 };
 const int kNumCutmaxVariants = sizeof(kCutmaxVariants) / sizeof(kCutmaxVariants[0]);
 

@@ -7,7 +7,7 @@
 //   2. Registers: xt_i = x_i + G_i, G_i = u_i^(1/alpha) (Beta) or -log(-log u_i)
 //      (Gumbel), u_i from Philox4x32-10 keyed by seed ^ row.
 //      Two consecutive elements share one Philox call.  Local max of x.
-//   3. cutmax_core on xt (identical code to the CutMax kernel).
+//   3. input_pass + cutmax_iterate on xt (identical code to the CutMax kernel).
 //   4. token = argmax Z, all-gathered across the cluster together with x_tok
 //      and max(x) (one 32-byte record per CTA pushed to every CTA).
 //   5. One pass over x (shared memory): e = exp(x - max x), sums of e and of
@@ -58,7 +58,6 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
   const int64_t base = (int64_t)rank * a.L;
   const int64_t rem = n - base;
   const int len = rem <= 0 ? 0 : (rem < a.L ? (int)rem : a.L);
-  const double mphantom = (double)((int64_t)C * NT * E - n);
   const uint32_t bar_load = ptx::smem_addr(&cb->mb_load);
   const uint32_t load_bytes = (uint32_t)len * 8u;
   const uint64_t policy = ptx::policy_evict_first();
@@ -127,7 +126,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
             v[k * VEC + j] = xv + v[k * VEC + j];
             xmax = fmax(xmax, xv);
           } else {
-            v[k * VEC + j] = K0;  // phantom (see cutmax_core)
+            v[k * VEC + j] = K0;  // phantom (see cutmax_iterate)
           }
         }
       }
@@ -135,9 +134,14 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
 
     double rnorm = 1.0;
     long long unused_argmax;
-    PassToken<NT, 1> tok(0, 0);
-    int st = cutmax_core<double, NT, 1, E, P, false>(v, tok, K0, mphantom, a.rp, a.inv_n, cb, xround, rank, C, 0, tid, base,
-                                                  nullptr, rnorm, unused_argmax);
+    const double2 part = input_pass<double, E>(v, K0);
+    const double2 rin = cluster_sum2<NT>(part.x, part.y, cb, xround, rank, C, tid);
+    auto final_xch = [&](double sy, double& bv, long long& bi) -> double {
+      return cluster_reduce<NT, false>(sy, 0.0, bv, bi, cb, xround, rank, C, tid).x;
+    };
+    auto hooks = make_hooks(false, [](int) {}, [](int) {}, final_xch);
+    int st = cutmax_iterate<double, NT, E, P, false>(v, rin.x, rin.y, K0, len, (double)((int64_t)C * NT * E - n), a.rp, a.inv_n, cb, xround, rank, C,
+                                                     tid, base, nullptr, rnorm, unused_argmax, hooks, nullptr);
 
     // token candidate over Z = Y * rnorm (and optional one-hot store)
     double best = -HUGE_VAL, bestx = 0.0;
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
         }
       }
     }
-    const double2 ta = cluster_sum2<NT>(tot, above, cb, xround, rank, C, 0, tid);
+    const double2 ta = cluster_sum2<NT>(tot, above, cb, xround, rank, C, tid);
     if (rank == 0 && tid == 0) {
       if (a.token) a.token[row] = (st == PAM_OK) ? (int32_t)besti : -1;
       if (a.inside) a.inside[row] = (st == PAM_OK && ta.y < a.p_nucleus * ta.x) ? 1 : 0;

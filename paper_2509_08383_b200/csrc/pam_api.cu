@@ -40,53 +40,63 @@ struct Geometry {
   int L = 0;
 };
 
-bool parse_force(int elem_bytes, int* ntg, int* e, int* c, int* g) {
+// Dev override: PAM_FORCE_CFG_F64 / PAM_FORCE_CFG_F32 = "NTG,E,C".
+bool parse_force(int elem_bytes, int* ntg, int* e, int* c) {
   const char* s = getenv(elem_bytes == 8 ? "PAM_FORCE_CFG_F64" : "PAM_FORCE_CFG_F32");
   if (!s || !*s) return false;
-  *g = 1;
-  return sscanf(s, "%d,%d,%d,%d", ntg, e, c, g) >= 3;
+  return sscanf(s, "%d,%d,%d", ntg, e, c) == 3;
 }
+
+int buffer_bytes(const Variant& v) { return ((v.ntg * v.e * v.elem_bytes + 127) / 128) * 128; }
+int smem_bytes(const Variant& v) { return buffer_bytes(v) + (int)sizeof(ControlBlock); }
 
 int64_t slice_len(int64_t n, int C, int vec) { return ((n + C - 1) / C + vec - 1) / vec * vec; }
 
+int max_active_clusters(const void* fn, int nt, int C, int smem);
+
+// Launch geometry.  Candidates are every (variant, cluster size C = 1..16)
+// whose per-CTA capacity covers the slice ceil(n/C) with < 30% phantom waste.
+// They are ranked with the row-period model measured on B200 (tools/trace.py):
+//   cycles/row ~= 0.66 * slice  (fp64 passes + row-boundary swap)
+//              + 11600          (T+1 cluster exchanges + scalar chains)
+// times the number of concurrently resident rows (occupancy query).  Non
+// power-of-two clusters matter: 9-CTA clusters pack 135 SMs vs 120 for 8.
 Geometry choose_geometry(int elem_bytes, int64_t B, int64_t n) {
   Geometry g;
   const int vec = 16 / elem_bytes;
-  int fntg, fe, fc, fg;
-  if (parse_force(elem_bytes, &fntg, &fe, &fc, &fg)) {
+  int fntg, fe, fc;
+  if (parse_force(elem_bytes, &fntg, &fe, &fc)) {
     for (int i = 0; i < kNumCutmaxVariants; ++i) {
       const Variant& v = kCutmaxVariants[i];
-      if (v.elem_bytes == elem_bytes && v.ntg == fntg && v.e == fe && v.g == fg) {
+      if (v.elem_bytes == elem_bytes && v.ntg == fntg && v.e == fe) {
         const int64_t L = slice_len(n, fc, vec);
         if ((int64_t)v.ntg * v.e >= L) { g.var = &v; g.C = fc; g.L = (int)L; return g; }
       }
     }
   }
-  (void)B;
-  // Measured preferences (tools/tune.py on B200): per-CTA slices of 256x76
-  // fp32 (two CTAs per SM) beat 512x40 (one per SM) for rows of >= 64K floats.
-  if (elem_bytes == 4 && n >= 65536) {
-    for (int i = 0; i < kNumCutmaxVariants; ++i) {
-      const Variant& v = kCutmaxVariants[i];
-      if (v.elem_bytes == 4 && v.ntg == 256 && v.e == 76 && v.g == 1) {
-        for (int C = 1; C <= 16; C *= 2) {
-          const int64_t L = slice_len(n, C, vec);
-          if ((int64_t)v.ntg * v.e >= L) { g.var = &v; g.C = C; g.L = (int)L; return g; }
-        }
-      }
-    }
-  }
-  for (int C = 1; C <= 16; C *= 2) {
+  int dev = 0;
+  const bool have_gpu = cudaGetDevice(&dev) == cudaSuccess;
+  double best_score = -1.0;
+  for (int C = 1; C <= 16; ++C) {
     const int64_t L = slice_len(n, C, vec);
-    const Variant* best = nullptr;
     for (int i = 0; i < kNumCutmaxVariants; ++i) {
       const Variant& v = kCutmaxVariants[i];
-      if (v.elem_bytes != elem_bytes || v.g != 1) continue;
-      if ((int64_t)v.ntg * v.e < L) continue;
-      if (!best || (int64_t)v.ntg * v.e < (int64_t)best->ntg * best->e) best = &v;
+      if (v.elem_bytes != elem_bytes) continue;
+      const int64_t cap = (int64_t)v.ntg * v.e;
+      if (cap < L || (C > 1 && cap > L + L * 3 / 10)) continue;
+      if (C > 1 && L < 2048) continue;  // tiny slices: exchanges would dominate
+      const int smem = smem_bytes(v);
+      if (smem > 227 * 1024) continue;
+      int active = 1;
+      if (have_gpu) active = max_active_clusters(v.fn[1], v.ntg, C, smem);
+      if (active <= 0) continue;
+      const int64_t rows_live = (B < active) ? B : active;
+      const double cyc = 0.66 * (double)L * (elem_bytes == 8 ? 1.0 : 0.6) + 11600.0;
+      const double score = (double)rows_live / cyc - 1e-9 * (double)C;  // tie-break: smaller clusters
+      if (score > best_score) { best_score = score; g.var = &v; g.C = C; g.L = (int)L; }
     }
-    if (best) { g.var = best; g.C = C; g.L = (int)L; return g; }
   }
+  cudaGetLastError();
   return g;
 }
 
@@ -199,17 +209,16 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   const int vec = 16 / (int)sizeof(Elem);
   const bool tma = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_z % 16 == 0) && (ld_x % vec == 0) &&
                    (ld_z % vec == 0) && (n % vec == 0) && getenv("PAM_DISABLE_TMA") == nullptr;
-  bool p3 = true;
+  bool p3 = getenv("PAM_FORCE_GENERIC_P") == nullptr;  // dev knob: A/B the generic-p kernel
   for (int t = 0; t < prm->T; ++t) p3 = p3 && (prm->p[t] == 3);
   const void* fn = g.var->fn[p3 ? 1 : 0];
-  const int G = g.var->g;
-  const int buf_bytes = tma ? ((g.L * (int)sizeof(Elem) + 127) / 128) * 128 : 0;
-  const int smem = G * (buf_bytes + (int)sizeof(ControlBlock));
-  const int nt = g.var->ntg * G;
+  // the row buffer is sized for the full capacity even without TMA so the
+  // occupancy (and the chooser's estimate) does not depend on alignment
+  const int smem = smem_bytes(*g.var);
+  const int nt = g.var->ntg;
   const int maxcl = max_active_clusters(fn, nt, g.C, smem);
   if (maxcl <= 0) return cuda_fail(cudaErrorInvalidConfiguration, "no cluster fits (occupancy 0)");
-  const int64_t want = (B + G - 1) / G;
-  const int clusters = (int)(want < maxcl ? want : maxcl);
+  const int clusters = (int)(B < maxcl ? B : maxcl);
   CutmaxArgs ka;
   memset(&ka, 0, sizeof ka);
   ka.x = d_x;
@@ -222,13 +231,10 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   ka.B = B;
   ka.n = n;
   ka.L = g.L;
-  ka.buf_bytes = buf_bytes;
-  ka.ctrl_offset = G * buf_bytes;
+  ka.ctrl_offset = buffer_bytes(*g.var);
   ka.tma = tma ? 1 : 0;
   ka.inv_n = 1.0 / (double)n;
   {
-    const char* sg = getenv("PAM_STAGGER");
-    ka.stagger = sg ? atoll(sg) : 0;
     const char* df = getenv("PAM_DEBUG_FLAGS");
     ka.debug_flags = df ? atoi(df) : 0;
   }
@@ -520,19 +526,16 @@ int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_par
   if (prm)
     for (int t = 0; t < prm->T; ++t) p3 = p3 && (prm->p[t] == 3);
   const void* fn = g.var->fn[p3 ? 1 : 0];
-  const int G = g.var->g;
-  const int buf_bytes = ((g.L * dtype_bytes + 127) / 128) * 128;
-  const int smem = G * (buf_bytes + (int)sizeof(ControlBlock));
-  info->threads = g.var->ntg * G;
+  const int smem = smem_bytes(*g.var);
+  info->threads = g.var->ntg;
   info->elems_per_thread = g.var->e;
   info->cluster = g.C;
   info->smem_bytes = smem;
   info->tma = 1;
   const int maxcl = max_active_clusters(fn, info->threads, g.C, smem);
-  const int64_t want = (B + G - 1) / G;
-  info->clusters = (int)(want < maxcl ? want : maxcl);
+  info->clusters = (int)(B < maxcl ? B : maxcl);
   info->ctas = info->clusters * g.C;
-  info->groups = G;
+  info->groups = 1;
   info->kernel_id = (int)(g.var - kCutmaxVariants);
   return PAM_OK;
 }

@@ -6,7 +6,7 @@
 namespace pam {
 
 struct Variant {
-  int elem_bytes, ntg, g, e;  // threads per row group, row groups per CTA, elements per thread
+  int elem_bytes, ntg, e;  // threads per CTA, elements per thread
   const void* fn[2];          // [P==3]
 };
 

@@ -1,21 +1,42 @@
-"""Per-phase timing of the CutMax kernel from the debug trace buffer (dev tool)."""
+"""Per-phase timing of the CutMax kernel from the debug trace buffer (dev tool).
+Needs the trace build:  make -C paper_2509_08383_b200/csrc trace  and
+PAM_LIB_PATH=paper_2509_08383_b200/libpam_trace.so  (set below if present)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("PAM_LIB_PATH", os.path.join(ROOT, "paper_2509_08383_b200", "libpam_trace.so"))
 import numpy as np
 import torch
 import paper_2509_08383_b200 as pam
 from paper_2509_08383_b200 import workloads as W
 
-NAMES = {0: "row start", 1: "TMA wait done", 2: "LDS+sync+next TMA", 3: "input pass", 4: "xchg0",
-         20: "core done (normaliser)", 21: "final pass (Z, stores)", 22: "argmax gather"}
-for t in range(8):
-    NAMES[5 + 2 * t] = f"iter{t} pass"; NAMES[6 + 2 * t] = f"iter{t} xchg"
+CLK = 1.965e3  # cycles per us (SM clock under load)
 
-def run(B, n, dtype, cfg=None):
+
+def names(T):  # p = 3 analytic-normaliser flow (the headline kernel)
+    nm = {2: "input pass + xchg (1st row)", 4: "input moments"}
+    for t in range(T - 1):
+        nm[5 + 2 * t] = f"chain + pass {t}" + (" (+3rd moment)" if t == T - 2 else "")
+        nm[6 + 2 * t] = f"xchg {t}"
+    nm.update({22: "chain + normaliser", 23: "X(next) wait", 24: "fused last pass + swap",
+               6 + 2 * (T - 1): "closing xchg", 21: "status"})
+    return nm
+
+
+def seq(T):
+    s = [0, 2, 4]
+    for t in range(T - 1):
+        s += [5 + 2 * t, 6 + 2 * t]
+    s += [22, 23, 24, 6 + 2 * (T - 1), 21]
+    return s
+
+
+def run(B, n, dtype, cfg=None, T=4):
+    key = "PAM_FORCE_CFG_F64" if dtype == torch.float64 else "PAM_FORCE_CFG_F32"
     if cfg:
-        os.environ["PAM_FORCE_CFG_F64" if dtype == torch.float64 else "PAM_FORCE_CFG_F32"] = cfg
+        os.environ[key] = cfg
     x = W.torch_gaussian(B, n, seed=1, dtype=dtype)
-    prm = pam.CutMaxParams()
+    prm = pam.CutMaxParams(T=T)
     info = pam.launch_info(x.element_size(), B, n, prm)
     buf = torch.zeros(info["ctas"] * 8 * 32, dtype=torch.int64, device="cuda")
     lib = pam._abi.load()
@@ -24,28 +45,25 @@ def run(B, n, dtype, cfg=None):
     pam.cutmax_batch_device(x, prm); torch.cuda.synchronize()
     lib.pam_set_trace_buffer(None, 0)
     tr = buf.view(info["ctas"], 8, 32).cpu().numpy().astype(np.float64)
-    ev = [0, 1, 2, 3, 4] + [k for t in range(4) for k in (5 + 2 * t, 6 + 2 * t)] + [20, 21, 22]
-    print(f"== B={B} n={n} {dtype} cfg={info['threads']}x{info['elems_per_thread']} G={info['groups']} C={info['cluster']} ctas={info['ctas']}")
-    rows = tr[:, 1:7, :]  # skip the first row (cold)
-    d = {}
-    for a, b in zip(ev, ev[1:]):
-        dd = rows[:, :, b] - rows[:, :, a]
-        d[(a, b)] = np.median(dd)
-    nxt = tr[:, 2:8, 0] - tr[:, 1:7, 22]
-    tot = np.median(tr[:, 2:8, 0] - tr[:, 1:7, 0])
-    for (a, b), v in d.items():
-        print(f"   {NAMES.get(b, b):28s} {v:8.0f} cyc  {v/1.965e3:7.2f} us  {100*v/tot:5.1f}%")
-    print(f"   {'gap to next row':28s} {np.median(nxt):8.0f} cyc")
-    for a, b, nm in ((3, 24, "xchg0: warp tree + push"), (24, 25, "xchg0: mbarrier wait"), (25, 26, "xchg0: slot reduce"),
-                     (26, 4, "xchg0: return"), (4, 28, "  guard"), (28, 29, "  loop top/status"), (29, 30, "  invsqrt"), (30, 27, "  k, b"), (4, 27, "scalar math (iter0)")):
-        print(f"   {nm:28s} {np.median(rows[:, :, b] - rows[:, :, a]):8.0f} cyc")
-    sk = tr[:, 1:7, 24].reshape(-1, info['cluster'], 6) if False else None
-    print(f"   {'row period':28s} {tot:8.0f} cyc  {tot/1.965e3:7.2f} us")
-    os.environ.pop("PAM_FORCE_CFG_F64", None); os.environ.pop("PAM_FORCE_CFG_F32", None)
+    print(f"== B={B} n={n} {dtype} T={T} cfg={info['threads']}x{info['elems_per_thread']} C={info['cluster']} "
+          f"ctas={info['ctas']}")
+    rows = tr[:, 1:7, :]  # skip the first (cold) row and the last
+    nm = names(T)
+    s = seq(T)
+    period = np.median(tr[:, 2:8, 0] - tr[:, 1:7, 0])
+    for a, b in zip(s, s[1:]):
+        v = np.median(rows[:, :, b] - rows[:, :, a])
+        print(f"   {nm.get(b, b):28s} {v:8.0f} cyc  {v / CLK:6.2f} us  {100 * v / period:5.1f}%")
+    for a, b, nm in ((0, 25, "DMA: hook ex0 done (half X(next))"), (0, 26, "DMA: hook ex1 done (all X(next))"),
+                     (0, 23, "X(next) landed (last pass start)")):
+        print(f"   {nm:28s} at {np.median(rows[:, :, b] - rows[:, :, a]):8.0f} cyc after row start")
+    print(f"   {'-> next row start':28s} {np.median(tr[:, 2:8, 0] - tr[:, 1:7, 21]):8.0f} cyc")
+    print(f"   {'row period':28s} {period:8.0f} cyc  {period / CLK:6.2f} us")
+    os.environ.pop(key, None)
 
-run(4096, 151936, torch.float64)
-run(4096, 151936, torch.float64, "256,38,16,2")
-run(4096, 32768, torch.float64, "256,38,4,2")
-run(4096, 32768, torch.float64)
-run(4096, 151936, torch.float32)
-run(4096, 1024, torch.float64)
+
+if __name__ == "__main__":
+    run(4096, 151936, torch.float64)
+    run(4096, 151936, torch.float64, "512,38,8")
+    run(4096, 32768, torch.float64)
+    run(4096, 151936, torch.float32)

@@ -6,10 +6,8 @@ import torch
 import paper_2509_08383_b200 as pam
 from paper_2509_08383_b200 import workloads as W
 
-VARS = {8: [(64,2,1),(128,4,1),(128,8,1),(256,8,1),(256,16,1),(512,16,1),(256,38,1),(512,24,1),(512,38,1),
-            (128,8,2),(256,16,2),(256,24,2),(256,38,2)],
-        4: [(64,4,1),(128,8,1),(256,8,1),(256,16,1),(512,16,1),(256,40,1),(512,24,1),(512,40,1),(256,76,1),
-            (256,16,2),(256,40,2),(256,76,2)]}
+VARS = {8: [(64,2),(128,4),(128,8),(256,8),(256,16),(512,16),(256,38),(512,24),(512,30),(512,34),(512,38)],
+        4: [(64,4),(128,8),(256,8),(256,16),(512,16),(256,40),(512,24),(512,40),(256,76)]}
 
 def bench(x, prm, reps=5):
     z = torch.empty_like(x); B = x.shape[0]
@@ -22,23 +20,6 @@ def bench(x, prm, reps=5):
     e1.record(); torch.cuda.synchronize()
     ok = bool(torch.equal(am.long(), x.argmax(dim=1))) and int((st != 0).sum()) == 0
     return e0.elapsed_time(e1) / reps, ok
-
-def stagger_sweep():
-    prm = pam.CutMaxParams()
-    for B, n, dt, cfgs in [(4096, 151936, torch.float64, ["512,38,8,1", "256,38,16,1", "256,38,16,2"]),
-                           (4096, 151936, torch.float32, ["256,76,8,1", "256,76,8,2"]),
-                           (4096, 32768, torch.float64, ["512,38,2,1", "256,38,4,1", "256,38,4,2"])]:
-        x = W.torch_gaussian(B, n, seed=1, dtype=dt)
-        esz = x.element_size()
-        key = "PAM_FORCE_CFG_F64" if esz == 8 else "PAM_FORCE_CFG_F32"
-        for cfg in cfgs:
-            os.environ[key] = cfg
-            for st in (0, 5000, 10000, 20000, 30000, 45000):
-                os.environ["PAM_STAGGER"] = str(st)
-                ms, ok = bench(x, prm)
-                gbs = B * (2 * n * esz + 4) / ms / 1e6
-                print(f"B={B} n={n} {dt} cfg={cfg:12s} stagger={st:6d}  {ms:8.4f} ms {gbs:7.1f} GB/s {100*gbs/6540.2:5.1f}% ok={ok}", flush=True)
-        os.environ.pop(key, None); os.environ.pop("PAM_STAGGER", None)
 
 def tsweep():
     for B, n, dt in [(4096, 151936, torch.float64), (4096, 32768, torch.float64)]:
@@ -53,23 +34,25 @@ def tsweep():
 def main():
     if len(sys.argv) > 1 and sys.argv[1] == "tsweep":
         return tsweep()
-    if len(sys.argv) > 1 and sys.argv[1] == "stagger":
-        return stagger_sweep()
     shapes = [(4096, 151936, torch.float64), (4096, 151936, torch.float32), (4096, 32768, torch.float64),
               (4096, 32768, torch.float32), (4096, 1024, torch.float64), (256, 151936, torch.float64),
               (64, 151936, torch.float64)]
-    if len(sys.argv) > 1: shapes = shapes[:int(sys.argv[1])]
+    if len(sys.argv) > 1:
+        sel = sys.argv[1]
+        # "5" = first five shapes; "@0,2" = shapes 0 and 2
+        shapes = [shapes[int(i)] for i in sel[1:].split(",")] if sel.startswith("@") else shapes[:int(sel)]
     prm = pam.CutMaxParams()
     for B, n, dt in shapes:
         x = W.torch_gaussian(B, n, seed=1, dtype=dt)
         esz = x.element_size(); vec = 16 // esz
         key = "PAM_FORCE_CFG_F64" if esz == 8 else "PAM_FORCE_CFG_F32"
         res = []
-        for C in (1, 2, 4, 8, 16):
+        for C in range(1, 17):
             L = ((n + C - 1) // C + vec - 1) // vec * vec
-            for nt, e, G in VARS[esz]:
-                if nt * e < L or nt * e > 2 * L: continue
-                os.environ[key] = f"{nt},{e},{C},{G}"
+            for nt, e in VARS[esz]:
+                G = 1
+                if nt * e < L or nt * e > 1.3 * L: continue
+                os.environ[key] = f"{nt},{e},{C}"
                 try:
                     ms, ok = bench(x, prm)
                     info = pam.launch_info(esz, B, n, prm)
@@ -79,7 +62,9 @@ def main():
                 res.append((gbs, nt, e, C, G, ms, ok, info['clusters'], info['ctas']))
         os.environ.pop(key, None)
         res.sort(reverse=True)
-        print(f"== B={B} n={n} {dt}")
+        ms_auto, _ = bench(x, prm)
+        ia = pam.launch_info(esz, B, n, prm)
+        print(f"== B={B} n={n} {dt}  [auto: {ia['threads']}x{ia['elems_per_thread']} C={ia['cluster']} -> {B*(2*n*esz+4)/ms_auto/1e6/65.402:.1f}%]")
         for gbs, nt, e, C, G, ms, ok, ncl, ctas in res:
             print(f"   NTG={nt:4d} E={e:3d} C={C:2d} G={G}  {ms:8.4f} ms  {gbs:7.1f} GB/s  {100*gbs/6540.2:5.1f}%  clusters={ncl} ctas={ctas} ok={ok}", flush=True)
 
