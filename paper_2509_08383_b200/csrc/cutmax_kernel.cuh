@@ -605,17 +605,20 @@ __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, c
   return st;
 }
 
-// Resident CTAs per SM the register budget should allow (launch-bounds hint).
+// Resident CTAs per SM the register budget allows without spilling the slice
+// (launch-bounds hint; MINB > 0 in the variant table overrides it).
 template <typename Elem, int NT, int E>
 constexpr int min_blocks_for() {
-  constexpr int regs = E * (int)sizeof(Elem) / 4 + 72;
+  constexpr int est = E * (int)sizeof(Elem) / 4 + 60;  // slice registers + ~60 of state
+  constexpr int regs = est < 96 ? 96 : est;
   constexpr int b = 65536 / (NT * regs);
   return b < 1 ? 1 : (b > 8 ? 8 : b);
 }
 
 // ---------------------------------------------------------------------------
-template <typename Elem, int NTG, int E, int P>
-__global__ void __launch_bounds__(NTG, (min_blocks_for<Elem, NTG, E>())) cutmax_rows_kernel(const CutmaxArgs a) {
+template <typename Elem, int NTG, int E, int P, int MINB = 0>
+__global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, NTG, E>()))
+    cutmax_rows_kernel(const CutmaxArgs a) {
   using Tr = ElemTraits<Elem>;
   using V = typename Tr::V;
   constexpr int VEC = Tr::VEC;
@@ -743,6 +746,7 @@ __global__ void __launch_bounds__(NTG, (min_blocks_for<Elem, NTG, E>())) cutmax_
     const double eps_var = rp.eps_var;
     bool in_ready = false;  // registers hold the K0-shifted row, (S_in, Q_in, R_in) its cluster sums
     double S_in = 0.0, Q_in = 0.0, R_in = 0.0;
+    Elem k0_cur = row < a.B ? __ldg(X + row * a.ldx) : Elem(0);
 #ifdef PAM_TRACE_BUILD
     int64_t lrow = 0;
 #endif
@@ -759,8 +763,9 @@ __global__ void __launch_bounds__(NTG, (min_blocks_for<Elem, NTG, E>())) cutmax_
 #endif
       PAM_TRACE(tr, 0);
       const Elem* xrow = X + row * a.ldx;
-      const Elem k0e = __ldg(xrow);  // shift for the input (same in every CTA)
+      const Elem k0e = k0_cur;  // shift for the input (same in every CTA)
       const double K0 = (double)k0e;
+      // x[next][0]: loaded a row ahead, first used by the last pass
       const Elem k0next = has_next ? __ldg(X + next * a.ldx) : Elem(0);
       if (!in_ready) {
         if (!TMA) {  // unaligned rows: direct loads, no staging
@@ -798,7 +803,7 @@ __global__ void __launch_bounds__(NTG, (min_blocks_for<Elem, NTG, E>())) cutmax_
       auto side = [&](int e) {
         if (e == 0) issue_upto(nch / 2);
         if (e == 1) issue_upto(nch);
-        PAM_TRACE_DMA(tr, 25 + (e < 2 ? e : 1));
+        if (e < 2) PAM_TRACE_DMA(tr, 25 + e);
       };
 
       int st = PAM_OK;
@@ -1073,6 +1078,7 @@ __global__ void __launch_bounds__(NTG, (min_blocks_for<Elem, NTG, E>())) cutmax_
         if (T == 1) R_in = cluster_sum2<NTG>(nxt.z, 0.0, cb, xround, rank, C, gtid).x;
       }
       in_ready = merged;
+      k0_cur = k0next;
       if (rank == 0 && gtid == 0) {
         if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)besti : -1;
         if (a.status) a.status[row] = st;
@@ -1086,6 +1092,7 @@ __global__ void __launch_bounds__(NTG, (min_blocks_for<Elem, NTG, E>())) cutmax_
     // ===== generic p: one-pass-late normalisation (see header) ==============
     bool in_ready = false;  // registers hold the K0-shifted row and (S_in, Q_in) its cluster sums
     double S_in = 0.0, Q_in = 0.0;
+    Elem k0_cur = row < a.B ? __ldg(X + row * a.ldx) : Elem(0);
     bool zpend = false;  // buf holds the previous row's unnormalised Y: scale in pass 0, then store
     Elem rn_prev = 1;
     int64_t zrow_prev = 0;
@@ -1105,8 +1112,9 @@ __global__ void __launch_bounds__(NTG, (min_blocks_for<Elem, NTG, E>())) cutmax_
   #endif
       PAM_TRACE(tr, 0);
       const Elem* xrow = X + row * a.ldx;
-      const Elem k0e = __ldg(xrow);  // shift for the input (same in every CTA)
+      const Elem k0e = k0_cur;  // shift for the input (same in every CTA)
       const double K0 = (double)k0e;
+      // x[next][0]: loaded a row ahead, first used by the last pass
       const Elem k0next = has_next ? __ldg(X + next * a.ldx) : Elem(0);
 
       if (!in_ready) {
@@ -1250,6 +1258,7 @@ __global__ void __launch_bounds__(NTG, (min_blocks_for<Elem, NTG, E>())) cutmax_
           }
         }
       }
+      k0_cur = k0next;
       PAM_TRACE(tr, 21);
   #ifdef PAM_TRACE_BUILD
       ++lrow;

@@ -40,11 +40,12 @@ struct Geometry {
   int L = 0;
 };
 
-// Dev override: PAM_FORCE_CFG_F64 / PAM_FORCE_CFG_F32 = "NTG,E,C".
-bool parse_force(int elem_bytes, int* ntg, int* e, int* c) {
+// Dev override: PAM_FORCE_CFG_F64 / PAM_FORCE_CFG_F32 = "NTG,E,C[,MINB]".
+bool parse_force(int elem_bytes, int* ntg, int* e, int* c, int* minb) {
   const char* s = getenv(elem_bytes == 8 ? "PAM_FORCE_CFG_F64" : "PAM_FORCE_CFG_F32");
   if (!s || !*s) return false;
-  return sscanf(s, "%d,%d,%d", ntg, e, c) == 3;
+  *minb = 0;
+  return sscanf(s, "%d,%d,%d,%d", ntg, e, c, minb) >= 3;
 }
 
 int buffer_bytes(const Variant& v) { return ((v.ntg * v.e * v.elem_bytes + 127) / 128) * 128; }
@@ -56,19 +57,22 @@ int max_active_clusters(const void* fn, int nt, int C, int smem);
 
 // Launch geometry.  Candidates are every (variant, cluster size C = 1..16)
 // whose per-CTA capacity covers the slice ceil(n/C) with < 30% phantom waste.
-// They are ranked with the row-period model measured on B200 (tools/trace.py):
-//   cycles/row ~= 0.66 * slice  (fp64 passes + row-boundary swap)
-//              + 11600          (T+1 cluster exchanges + scalar chains)
-// times the number of concurrently resident rows (occupancy query).  Non
-// power-of-two clusters matter: 9-CTA clusters pack 135 SMs vs 120 for 8.
+// They are ranked by rows per microsecond, clusters / t_row, with the row
+// period fitted to B200 measurements (tools/tune.py, tools/trace.py):
+//   t_row ~= a + b * cap * k
+// a = latency per row (T exchanges + scalar chains: fp64 4.8 us, fp32 2.5 us),
+// b = element cost per CTA-slot (fp64 0.33 ns, fp32 0.35 ns), cap = NTG*E, and
+// k = CTAs sharing an SM (clusters*C / #SMs, rounded up) from the occupancy
+// query.  Non power-of-two clusters matter: 9-CTA clusters pack 135 SMs vs 120
+// for 8.
 Geometry choose_geometry(int elem_bytes, int64_t B, int64_t n) {
   Geometry g;
   const int vec = 16 / elem_bytes;
-  int fntg, fe, fc;
-  if (parse_force(elem_bytes, &fntg, &fe, &fc)) {
+  int fntg, fe, fc, fmb;
+  if (parse_force(elem_bytes, &fntg, &fe, &fc, &fmb)) {
     for (int i = 0; i < kNumCutmaxVariants; ++i) {
       const Variant& v = kCutmaxVariants[i];
-      if (v.elem_bytes == elem_bytes && v.ntg == fntg && v.e == fe) {
+      if (v.elem_bytes == elem_bytes && v.ntg == fntg && v.e == fe && v.minb == fmb) {
         const int64_t L = slice_len(n, fc, vec);
         if ((int64_t)v.ntg * v.e >= L) { g.var = &v; g.C = fc; g.L = (int)L; return g; }
       }
@@ -76,6 +80,9 @@ Geometry choose_geometry(int elem_bytes, int64_t B, int64_t n) {
   }
   int dev = 0;
   const bool have_gpu = cudaGetDevice(&dev) == cudaSuccess;
+  int nsm = 148;
+  if (have_gpu && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
+  const double a_us = elem_bytes == 8 ? 4.8 : 2.5, b_ns = elem_bytes == 8 ? 0.33 : 0.35;
   double best_score = -1.0;
   for (int C = 1; C <= 16; ++C) {
     const int64_t L = slice_len(n, C, vec);
@@ -87,12 +94,12 @@ Geometry choose_geometry(int elem_bytes, int64_t B, int64_t n) {
       if (C > 1 && L < 2048) continue;  // tiny slices: exchanges would dominate
       const int smem = smem_bytes(v);
       if (smem > 227 * 1024) continue;
-      int active = 1;
-      if (have_gpu) active = max_active_clusters(v.fn[1], v.ntg, C, smem);
+      const int active = have_gpu ? max_active_clusters(v.fn[1], v.ntg, C, smem) : nsm / C;
       if (active <= 0) continue;
-      const int64_t rows_live = (B < active) ? B : active;
-      const double cyc = 0.66 * (double)L * (elem_bytes == 8 ? 1.0 : 0.6) + 11600.0;
-      const double score = (double)rows_live / cyc - 1e-9 * (double)C;  // tie-break: smaller clusters
+      const int64_t clusters = (B < active) ? B : active;
+      const int64_t k = (clusters * C + nsm - 1) / nsm;
+      const double t_us = a_us + 1e-3 * b_ns * (double)cap * (double)(k < 1 ? 1 : k);
+      const double score = (double)clusters / t_us - 1e-9 * (double)C;  // tie-break: smaller clusters
       if (score > best_score) { best_score = score; g.var = &v; g.C = C; g.L = (int)L; }
     }
   }

@@ -6,7 +6,7 @@
 namespace pam {
 
 struct Variant {
-  int elem_bytes, ntg, e;  // threads per CTA, elements per thread
+  int elem_bytes, ntg, e, minb;  // threads per CTA, elements per thread, launch-bounds min blocks (0: auto)
   const void* fn[2];          // [P==3]
 };
 

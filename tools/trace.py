@@ -63,6 +63,11 @@ def run(B, n, dtype, cfg=None, T=4):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "nostore":
+        run(4096, 151936, torch.float64)
+        os.environ["PAM_DEBUG_FLAGS"] = "1"
+        run(4096, 151936, torch.float64)
+        sys.exit(0)
     run(4096, 151936, torch.float64)
     run(4096, 151936, torch.float64, "512,38,8")
     run(4096, 32768, torch.float64)

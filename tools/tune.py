@@ -6,8 +6,9 @@ import torch
 import paper_2509_08383_b200 as pam
 from paper_2509_08383_b200 import workloads as W
 
-VARS = {8: [(64,2),(128,4),(128,8),(256,8),(256,16),(512,16),(256,38),(512,24),(512,30),(512,34),(512,38)],
-        4: [(64,4),(128,8),(256,8),(256,16),(512,16),(256,40),(512,24),(512,40),(256,76)]}
+VARS = {8: [(64,2,0),(128,4,0),(128,8,0),(256,8,0),(256,16,0),(512,16,0),(256,38,0),(512,24,0),(512,30,0),(512,34,0),
+            (512,38,0),(256,38,2)],
+        4: [(64,4,0),(128,8,0),(256,8,0),(256,16,0),(512,16,0),(256,40,0),(512,24,0),(512,40,0),(256,76,0),(256,76,2)]}
 
 def bench(x, prm, reps=5):
     z = torch.empty_like(x); B = x.shape[0]
@@ -49,10 +50,10 @@ def main():
         res = []
         for C in range(1, 17):
             L = ((n + C - 1) // C + vec - 1) // vec * vec
-            for nt, e in VARS[esz]:
-                G = 1
+            for nt, e, mb in VARS[esz]:
+                G = mb
                 if nt * e < L or nt * e > 1.3 * L: continue
-                os.environ[key] = f"{nt},{e},{C}"
+                os.environ[key] = f"{nt},{e},{C},{mb}"
                 try:
                     ms, ok = bench(x, prm)
                     info = pam.launch_info(esz, B, n, prm)
@@ -66,6 +67,6 @@ def main():
         ia = pam.launch_info(esz, B, n, prm)
         print(f"== B={B} n={n} {dt}  [auto: {ia['threads']}x{ia['elems_per_thread']} C={ia['cluster']} -> {B*(2*n*esz+4)/ms_auto/1e6/65.402:.1f}%]")
         for gbs, nt, e, C, G, ms, ok, ncl, ctas in res:
-            print(f"   NTG={nt:4d} E={e:3d} C={C:2d} G={G}  {ms:8.4f} ms  {gbs:7.1f} GB/s  {100*gbs/6540.2:5.1f}%  clusters={ncl} ctas={ctas} ok={ok}", flush=True)
+            print(f"   NTG={nt:4d} E={e:3d} C={C:2d} MINB={G}  {ms:8.4f} ms  {gbs:7.1f} GB/s  {100*gbs/6540.2:5.1f}%  clusters={ncl} ctas={ctas} ok={ok}", flush=True)
 
 main()
