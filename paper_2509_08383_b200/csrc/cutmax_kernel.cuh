@@ -89,6 +89,15 @@ struct __align__(16) XchRecord {
   double2 cand;  // (value, index bits)
 };
 
+// One exchange channel (the dual-row kernel runs two; ControlBlock embeds the
+// same members so the exchange templates take either).
+struct __align__(16) XchChannel {
+  XchRecord xch[2][16];  // slots per cluster rank, double-buffered by round parity
+  double2 wred[32];      // per-warp partial sums
+  double2 wcand[32];     // per-warp argmax candidates / third sums
+  unsigned long long mb_x[2];
+};
+
 struct __align__(16) ControlBlock {
   XchRecord xch[2][16];  // exchange slots per cluster rank, double-buffered by round parity
   double2 xin[16];       // next row's input sums per cluster rank (row-boundary exchange)
@@ -189,8 +198,8 @@ struct NoSide {
 // slot); or two sums plus the lexicographic (value desc, index asc) argmax.
 enum XchMode { kSum2 = 0, kSum3 = 1, kArgmax = 2 };
 
-template <int NTG, int MODE, typename Side = NoSide>
-__device__ __forceinline__ void xch_push(double a, double b, double c, long long ci_, ControlBlock* cb,
+template <int NTG, int MODE, typename Ch, typename Side = NoSide>
+__device__ __forceinline__ void xch_push(double a, double b, double c, long long ci_, Ch* cb,
                                          const uint32_t round, const uint32_t rank, const uint32_t C, const int gtid,
                                          const Side& side = Side()) {
   constexpr int NW = NTG / 32;
@@ -236,8 +245,8 @@ __device__ __forceinline__ void xch_push(double a, double b, double c, long long
 // xch_wait: wait for the C records of this round, re-arm the barrier for
 // round + 2 and combine the records (16-lane butterfly, same order everywhere).
 // Returns (a, b); c / ci receive the third sum or the argmax.
-template <int MODE>
-__device__ __forceinline__ double2 xch_wait(double& c, long long& ci, ControlBlock* cb, uint32_t& round,
+template <int MODE, typename Ch>
+__device__ __forceinline__ double2 xch_wait(double& c, long long& ci, Ch* cb, uint32_t& round,
                                             const uint32_t C, const int gtid) {
   const int lane = gtid & 31;
   const uint32_t par = round & 1u, ph = (round >> 1) & 1u;
@@ -263,8 +272,8 @@ __device__ __forceinline__ double2 xch_wait(double& c, long long& ci, ControlBlo
   return make_double2(a, b);
 }
 
-template <int NTG, bool ARGMAX>
-__device__ __forceinline__ double2 cluster_reduce(double a, double b, double& best, long long& besti, ControlBlock* cb,
+template <int NTG, bool ARGMAX, typename Ch>
+__device__ __forceinline__ double2 cluster_reduce(double a, double b, double& best, long long& besti, Ch* cb,
                                                   uint32_t& round, const uint32_t rank, const uint32_t C,
                                                   const int gtid) {
   constexpr int M = ARGMAX ? kArgmax : kSum2;
@@ -272,8 +281,8 @@ __device__ __forceinline__ double2 cluster_reduce(double a, double b, double& be
   return xch_wait<M>(best, besti, cb, round, C, gtid);
 }
 
-template <int NTG>
-__device__ __forceinline__ double2 cluster_sum2(double a, double b, ControlBlock* cb, uint32_t& round,
+template <int NTG, typename Ch>
+__device__ __forceinline__ double2 cluster_sum2(double a, double b, Ch* cb, uint32_t& round,
                                                 const uint32_t rank, const uint32_t C, const int gtid) {
   double bv = 0.0;
   long long bi = 0;
@@ -281,8 +290,8 @@ __device__ __forceinline__ double2 cluster_sum2(double a, double b, ControlBlock
 }
 
 // Three cluster sums in one exchange.
-template <int NTG>
-__device__ __forceinline__ double3 cluster_sum3(double a, double b, double c, ControlBlock* cb, uint32_t& round,
+template <int NTG, typename Ch>
+__device__ __forceinline__ double3 cluster_sum3(double a, double b, double c, Ch* cb, uint32_t& round,
                                                 const uint32_t rank, const uint32_t C, const int gtid) {
   long long ci = 0;
   xch_push<NTG, kSum3>(a, b, c, ci, cb, round, rank, C, gtid);
@@ -914,6 +923,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         w = cutmax_update<Elem, 3>(w, ke, be, kn, 3);
         const double kthis = knext;
         const bool need3 = (t + 2 == T);
+        PAM_TRACE(tr, 13 + t);
         double3 part;
         if (need3)
           pass(BoolC<true>(), ke, be, kn, part);
@@ -927,15 +937,18 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         double2 r;
         if (need3) {
           xch_push<NTG, kSum3>(part.x, part.y, part.z, 0LL, cb, xround, rank, C, gtid, [&]() { side(t); });
+          PAM_TRACE(tr, 16 + t);
           r = xch_wait<kSum3>(r3, ci, cb, xround, C, gtid);
         } else {
           xch_push<NTG, kSum2>(part.x, part.y, 0.0, 0LL, cb, xround, rank, C, gtid, [&]() { side(t); });
+          PAM_TRACE(tr, 16 + t);
           r = xch_wait<kSum2>(r3, ci, cb, xround, C, gtid);
         }
         PAM_TRACE(tr, 6 + 2 * t);
         const double wd = (double)w;
         moments(r.x - mph * wd, r.y - mph * wd * wd, r3 - mph * wd * wd * wd, wd, need3);
         kcur = kthis;
+        PAM_TRACE(tr, 27 + t);
       }
 
       // ---- last iteration: normaliser first, then the fused pass ---------------

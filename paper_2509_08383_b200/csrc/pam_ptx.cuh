@@ -128,14 +128,18 @@ __device__ __forceinline__ void bulk_s2g(void* gdst, uint32_t smem_src, uint32_t
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // Wait until all committed bulk stores of this thread have finished READING shared memory.
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-// Wait until at most n (0..3) of this thread's most recent bulk groups are
+// Wait until at most n (0..7) of this thread's most recent bulk groups are
 // still reading shared memory (the group count must be an immediate).
 __device__ __forceinline__ void bulk_wait_read_le(int n) {
   switch (n) {
     case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
     case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
     case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
-    default: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group.read 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.bulk.wait_group.read 6;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory"); break;
   }
 }
 // Wait until all committed bulk stores of this thread are complete.

@@ -16,8 +16,11 @@ CLK = 1.965e3  # cycles per us (SM clock under load)
 def names(T):  # p = 3 analytic-normaliser flow (the headline kernel)
     nm = {2: "input pass + xchg (1st row)", 4: "input moments"}
     for t in range(T - 1):
-        nm[5 + 2 * t] = f"chain + pass {t}" + (" (+3rd moment)" if t == T - 2 else "")
-        nm[6 + 2 * t] = f"xchg {t}"
+        nm[13 + t] = f"chain {t}"
+        nm[5 + 2 * t] = f"pass {t}" + (" (+3rd moment)" if t == T - 2 else "")
+        nm[16 + t] = f"push {t} (bfly+barrier+send)"
+        nm[6 + 2 * t] = f"wait {t} (+record combine)"
+        nm[27 + t] = f"moments {t}"
     nm.update({22: "chain + normaliser", 23: "X(next) wait", 24: "fused last pass + swap",
                6 + 2 * (T - 1): "closing xchg", 21: "status"})
     return nm
@@ -26,7 +29,7 @@ def names(T):  # p = 3 analytic-normaliser flow (the headline kernel)
 def seq(T):
     s = [0, 2, 4]
     for t in range(T - 1):
-        s += [5 + 2 * t, 6 + 2 * t]
+        s += [13 + t, 5 + 2 * t, 16 + t, 6 + 2 * t, 27 + t]
     s += [22, 23, 24, 6 + 2 * (T - 1), 21]
     return s
 
@@ -57,6 +60,12 @@ def run(B, n, dtype, cfg=None, T=4):
     for a, b, nm in ((0, 25, "DMA: hook ex0 done (half X(next))"), (0, 26, "DMA: hook ex1 done (all X(next))"),
                      (0, 23, "X(next) landed (last pass start)")):
         print(f"   {nm:28s} at {np.median(rows[:, :, b] - rows[:, :, a]):8.0f} cyc after row start")
+    # exchange latency spread over CTAs (pass end -> records combined, thread 0)
+    for t in range(T):
+        a_, b_ = (16 + t, 6 + 2 * t) if t < T - 1 else (24, 6 + 2 * t)
+        d = (rows[:, :, b_] - rows[:, :, a_]).ravel()
+        print(f"   xchg {t} wait spread: min {np.min(d):6.0f} p10 {np.percentile(d, 10):6.0f} med {np.median(d):6.0f} "
+              f"p90 {np.percentile(d, 90):6.0f} max {np.max(d):6.0f}")
     print(f"   {'-> next row start':28s} {np.median(tr[:, 2:8, 0] - tr[:, 1:7, 21]):8.0f} cyc")
     print(f"   {'row period':28s} {period:8.0f} cyc  {period / CLK:6.2f} us")
     os.environ.pop(key, None)
@@ -69,6 +78,4 @@ if __name__ == "__main__":
         run(4096, 151936, torch.float64)
         sys.exit(0)
     run(4096, 151936, torch.float64)
-    run(4096, 151936, torch.float64, "512,38,8")
     run(4096, 32768, torch.float64)
-    run(4096, 151936, torch.float32)
