@@ -98,8 +98,16 @@ struct __align__(16) XchChannel {
   unsigned long long mb_x[2];
 };
 
+// Coefficients the control warp publishes for the next pass (p = 3 flow).
+struct __align__(16) Bcast {
+  double ke, be, dm, re;
+  int flag;  // 1: the exact second pass about dm is needed first
+  int pad[3];
+};
+
 struct __align__(16) ControlBlock {
   XchRecord xch[2][16];  // exchange slots per cluster rank, double-buffered by round parity
+  Bcast bc;              // control-warp broadcast (p = 3 flow)
   double2 xin[16];       // next row's input sums per cluster rank (row-boundary exchange)
   double2 wred[32];      // per-warp partial sums (CTA pre-reduction; sampler token gather)
   double2 wcand[32];     // per-warp argmax candidates
@@ -150,6 +158,8 @@ __device__ __forceinline__ double fma_e(double a, double b, double c) { return f
 __device__ __forceinline__ float fma_e(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double ipow_e(double z, int p) { return ipow(z, p); }
 __device__ __forceinline__ float ipow_e(float z, int p) { return ipowf(z, p); }
+
+__device__ __forceinline__ int lane_of(int tid) { return tid & 31; }
 
 __device__ __forceinline__ bool cand_better(double v, long long i, double bv, long long bi) {
   return (v > bv) || (v == bv && i < bi);
@@ -747,15 +757,23 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
     // power sum rides on the exchange of pass T-2 (or the input for T = 1).
     // A non-finite analytic total (third powers overflowing) falls back to an
     // explicit sum of Y (extra pass + exchange).
+    //
+    // Control warp.  Between two passes only warp 0 waits for the exchange,
+    // combines the C records and runs the scalar chain (moments, status,
+    // 1/sigma, normaliser); it publishes the pass coefficients in shared memory
+    // and the other warps pick them up at a named barrier.  Replicating that
+    // latency-bound scalar work in all 16 warps cost ~25% of each gap.
     constexpr double kGuard = sizeof(Elem) == 8 ? 16.0 : 2.0;
+    const int warp = gtid >> 5;
     const double nd = (double)n;
     const double inv_n = a.inv_n;
     const bool normalize = !(rp.flags & PAM_F_NO_NORMALIZE);
     const bool poly_invsqrt = rp.invsqrt_mode == PAM_MODE_POLY;
     const double eps_var = rp.eps_var;
-    bool in_ready = false;  // registers hold the K0-shifted row, (S_in, Q_in, R_in) its cluster sums
-    double S_in = 0.0, Q_in = 0.0, R_in = 0.0;
+    bool in_ready = false;  // registers hold the K0-shifted row; warp 0 holds its cluster sums
+    double S_c = 0.0, Q_c = 0.0, R_c = 0.0;  // warp 0: cluster sums of the current iterate
     Elem k0_cur = row < a.B ? __ldg(X + row * a.ldx) : Elem(0);
+    auto bar1 = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(NTG) : "memory"); };
 #ifdef PAM_TRACE_BUILD
     int64_t lrow = 0;
 #endif
@@ -788,9 +806,9 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         }
         const double3 part = input_pass3<Elem, E>(v, K0);
         const double3 r = cluster_sum3<NTG>(part.x, part.y, part.z, cb, xround, rank, C, gtid);
-        S_in = r.x;
-        Q_in = r.y;
-        R_in = r.z;
+        S_c = r.x;
+        Q_c = r.y;
+        R_c = r.z;
       }
       PAM_TRACE(tr, 2);
 
@@ -815,11 +833,17 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         if (e < 2) PAM_TRACE_DMA(tr, 25 + e);
       };
 
+      // ---- warp 0's scalar state ---------------------------------------------------
       int st = PAM_OK;
       double dm = 0.0, s2 = 0.0, m3 = 0.0, e1 = 0.0;
-      // moments of the current iterate from its shifted cluster sums (+ the
-      // exact second pass when the one-pass form cancelled, see header)
-      auto moments = [&](double S, double Q, double R, double w, bool need3) {
+      double kcur = K0, c_inv = rp.inv_c[0], knext = rp.kshift[1];
+      Elem w = 0;  // phantom value (shifted representation)
+      double* stats_row = (rank == 0 && gtid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr;
+      if (!isfinite(S_c) || !isfinite(Q_c)) st = PAM_ERR_NON_FINITE;
+
+      // moments of iterate t from its (phantom-corrected) cluster sums; returns
+      // false when the one-pass form cancelled and the exact pass is needed
+      auto moments = [&](double S, double Q, double R, bool need3) -> bool {
         dm = S * inv_n;
         const double qn = Q * inv_n;
         s2 = fma(-dm, dm, qn);
@@ -827,38 +851,10 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
           e1 = fma(-nd, dm, S);
           m3 = fma(dm, fma(2.0 * dm, dm, -3.0 * qn), R * inv_n);
         }
-        if (st == PAM_OK && isfinite(Q) && qn > kGuard * s2) {
-          const Elem dme = (Elem)dm;
-          Elem q2a = 0, q2b = 0, r3a = 0, r3b = 0;
-#pragma unroll
-          for (int i = 0; i < E; i += 2) {
-            const Elem d0 = v[i] - dme, d1 = v[i + 1] - dme;
-            const Elem f0 = d0 * d0, f1 = d1 * d1;
-            if (real(i)) {
-              q2a += f0;
-              r3a = fma_e(f0, d0, r3a);
-            }
-            if (real(i + 1)) {
-              q2b += f1;
-              r3b = fma_e(f1, d1, r3b);
-            }
-          }
-          const double2 r2 =
-              cluster_sum2<NTG>((double)q2a + (double)q2b, (double)r3a + (double)r3b, cb, xround, rank, C, gtid);
-          const double dw = (double)((Elem)w - dme);
-          s2 = (r2.x - mph * dw * dw) * inv_n;
-          if (need3) m3 = (r2.y - mph * dw * dw * dw) * inv_n;
-        }
+        return !(st == PAM_OK && isfinite(Q) && qn > kGuard * s2);
       };
-      if (!isfinite(S_in) || !isfinite(Q_in)) st = PAM_ERR_NON_FINITE;
-      moments(S_in, Q_in, R_in, 0.0, T == 1);
-      PAM_TRACE(tr, 4);
-
-      double* stats_row = (rank == 0 && gtid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr;
-      double kcur = K0, c_inv = rp.inv_c[0], knext = rp.kshift[1];
-      double kd = 0.0, bd = 1.0;
-      // scalar chain of iteration t: status, k = inv_sigma / c, b = 1 - dm k
-      auto chain = [&](int t) {
+      // scalar chain of iteration t (+ the analytic normaliser for the last one)
+      auto chain = [&](int t, double& kd, double& bd, double& rnorm) {
         const double mu = kcur + dm;
         const bool bad_range = !isfinite(mu) || !isfinite(s2);
         st = (st != PAM_OK) ? st : (bad_range ? PAM_ERR_RANGE : (s2 < eps_var ? PAM_ERR_DEGENERATE_INPUT : PAM_OK));
@@ -879,9 +875,107 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         }
         kd = (st == PAM_OK) ? inv_sigma * c_inv : 0.0;
         bd = fma(-dm, kd, 1.0);
+        rnorm = 1.0;
+        if (t == T - 1) {
+          const double total = nd + kd * (3.0 * e1 + kd * (3.0 * nd * s2 + kd * nd * m3));
+          if (st == PAM_OK && !isfinite(total)) {
+            rnorm = NAN;  // explicit sum needed (rare): signalled to the CTA
+            return;
+          }
+          if (st == PAM_OK && normalize) {
+            if (!(total > 0.0)) {
+              st = PAM_ERR_RANGE;  // Z must be a distribution (pin A7)
+            } else if (rp.inv_mode == PAM_MODE_POLY) {
+              const pam_approx_config& ac = rp.inv;
+              const int rs = inv_rescaled(total, ac.iterations, ac.rescale, ac.scale_log2, ac.lo, ac.hi, &rnorm);
+              if (rs) st = rs;
+            } else {
+              rnorm = 1.0 / total;
+            }
+          }
+        }
+      };
+      // final normaliser from an explicit total (rare fallback)
+      auto finish_total = [&](double total, double& rnorm) {
+        rnorm = 1.0;
+        if (st == PAM_OK && !isfinite(total)) st = PAM_ERR_RANGE;
+        if (st == PAM_OK && normalize) {
+          if (!(total > 0.0)) {
+            st = PAM_ERR_RANGE;
+          } else if (rp.inv_mode == PAM_MODE_POLY) {
+            const pam_approx_config& ac = rp.inv;
+            const int rs = inv_rescaled(total, ac.iterations, ac.rescale, ac.scale_log2, ac.lo, ac.hi, &rnorm);
+            if (rs) st = rs;
+          } else {
+            rnorm = 1.0 / total;
+          }
+        }
+      };
+      // control step for pass t (warp 0 computes, everyone receives): returns the
+      // affine coefficients (ke, be) and, for the last pass, the normaliser re.
+      auto control = [&](int t, Elem& ke, Elem& be, Elem& re) {
+        const bool need3 = (t == T - 1);
+        if (warp == 0) {
+          const bool ok = moments(S_c, Q_c, R_c, need3);
+          Bcast& bc = cb->bc;
+          if (ok) {
+            double kd, bd, rn;
+            chain(t, kd, bd, rn);
+            if (lane_of(gtid) == 0) {
+              bc.ke = kd;
+              bc.be = bd;
+              bc.dm = dm;
+              bc.re = rn;
+              bc.flag = 0;
+            }
+          } else if (lane_of(gtid) == 0) {
+            bc.dm = dm;
+            bc.flag = 1;
+          }
+        }
+        bar1();
+        Bcast b = cb->bc;
+        if (b.flag) {  // exact second pass about dm (cluster-uniform, rare)
+          const Elem dme = (Elem)b.dm;
+          Elem q2a = 0, q2b = 0, r3a = 0, r3b = 0;
+#pragma unroll
+          for (int i = 0; i < E; i += 2) {
+            const Elem d0 = v[i] - dme, d1 = v[i + 1] - dme;
+            const Elem f0 = d0 * d0, f1 = d1 * d1;
+            if (real(i)) {
+              q2a += f0;
+              r3a = fma_e(f0, d0, r3a);
+            }
+            if (real(i + 1)) {
+              q2b += f1;
+              r3b = fma_e(f1, d1, r3b);
+            }
+          }
+          const double2 r2 =
+              cluster_sum2<NTG>((double)q2a + (double)q2b, (double)r3a + (double)r3b, cb, xround, rank, C, gtid);
+          if (warp == 0) {
+            const double dw = (double)((Elem)w - dme);
+            s2 = (r2.x - mph * dw * dw) * inv_n;
+            if (need3) m3 = (r2.y - mph * dw * dw * dw) * inv_n;
+            double kd, bd, rn;
+            chain(t, kd, bd, rn);
+            if (lane_of(gtid) == 0) {
+              cb->bc.ke = kd;
+              cb->bc.be = bd;
+              cb->bc.dm = dm;
+              cb->bc.re = rn;
+              cb->bc.flag = 0;
+            }
+          }
+          bar1();
+          b = cb->bc;
+        }
+        ke = (Elem)b.ke;
+        be = affine_coef<Elem>(b.be, b.dm);
+        re = (Elem)b.re;
+        // (bc is rewritten only after the next push's CTA barrier: no barrier here)
       };
 
-      Elem w = 0;  // phantom value (shifted representation)
       // pass t < T-1: update + shifted moments (+ third power sum on pass T-2)
       auto pass = [&](auto r_c, Elem ke, Elem be, Elem kn, double3& out) {
         constexpr bool R3 = decltype(r_c)::value;
@@ -917,72 +1011,66 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         }
         out = make_double3((double)sa + (double)sb, (double)qa + (double)qb, (double)ra + (double)rb);
       };
+
       for (int t = 0; t + 1 < T; ++t) {
-        chain(t);
-        const Elem ke = (Elem)kd, be = affine_coef<Elem>(bd, dm), kn = (Elem)(-knext);
-        w = cutmax_update<Elem, 3>(w, ke, be, kn, 3);
-        const double kthis = knext;
-        const bool need3 = (t + 2 == T);
+        Elem ke, be, re_unused;
+        control(t, ke, be, re_unused);
+        const Elem kn = (Elem)(-knext);
         PAM_TRACE(tr, 13 + t);
+        const bool need3 = (t + 2 == T);
         double3 part;
         if (need3)
           pass(BoolC<true>(), ke, be, kn, part);
         else
           pass(BoolC<false>(), ke, be, kn, part);
-        c_inv = rp.inv_c[t + 1];  // prefetch next iteration's constants
-        knext = rp.kshift[t + 2];
         PAM_TRACE(tr, 5 + 2 * t);
-        double r3 = 0.0;
-        long long ci = 0;
-        double2 r;
-        if (need3) {
+        if (need3)
           xch_push<NTG, kSum3>(part.x, part.y, part.z, 0LL, cb, xround, rank, C, gtid, [&]() { side(t); });
-          PAM_TRACE(tr, 16 + t);
-          r = xch_wait<kSum3>(r3, ci, cb, xround, C, gtid);
-        } else {
+        else
           xch_push<NTG, kSum2>(part.x, part.y, 0.0, 0LL, cb, xround, rank, C, gtid, [&]() { side(t); });
-          PAM_TRACE(tr, 16 + t);
-          r = xch_wait<kSum2>(r3, ci, cb, xround, C, gtid);
+        PAM_TRACE(tr, 16 + t);
+        if (warp == 0) {
+          double r3 = 0.0;
+          long long ci = 0;
+          const double2 r = need3 ? xch_wait<kSum3>(r3, ci, cb, xround, C, gtid)
+                                  : xch_wait<kSum2>(r3, ci, cb, xround, C, gtid);
+          w = cutmax_update<Elem, 3>(w, ke, be, kn, 3);
+          const double wd = (double)w;
+          S_c = r.x - mph * wd;
+          Q_c = r.y - mph * wd * wd;
+          R_c = r3 - mph * wd * wd * wd;
+          kcur = knext;
+          c_inv = rp.inv_c[t + 1];
+          knext = rp.kshift[t + 2];
+        } else {
+          ++xround;  // keep the round counter in step with warp 0
         }
         PAM_TRACE(tr, 6 + 2 * t);
-        const double wd = (double)w;
-        moments(r.x - mph * wd, r.y - mph * wd * wd, r3 - mph * wd * wd * wd, wd, need3);
-        kcur = kthis;
-        PAM_TRACE(tr, 27 + t);
       }
 
       // ---- last iteration: normaliser first, then the fused pass ---------------
-      chain(T - 1);
-      const Elem ke = (Elem)kd, be = affine_coef<Elem>(bd, dm), kz = (Elem)0;  // kshift[T] = 0
-      double rnorm = 1.0;
-      {
-        double total = nd + kd * (3.0 * e1 + kd * (3.0 * nd * s2 + kd * nd * m3));
-        if (st == PAM_OK && !isfinite(total)) {  // explicit sum (rare)
-          Elem ta = 0, tb = 0;
+      Elem ke, be, re;
+      control(T - 1, ke, be, re);
+      const Elem kz = (Elem)0;  // kshift[T] = 0
+      if (!(re == re)) {  // analytic total not finite: explicit sum of Y (rare, cluster-uniform)
+        Elem ta = 0, tb = 0;
 #pragma unroll
-          for (int i = 0; i < E; i += 2) {
-            const Elem y0 = cutmax_update<Elem, 3>(v[i], ke, be, kz, 3);
-            const Elem y1 = cutmax_update<Elem, 3>(v[i + 1], ke, be, kz, 3);
-            if (real(i)) ta += y0;
-            if (real(i + 1)) tb += y1;
-          }
-          total = cluster_sum2<NTG>((double)ta + (double)tb, 0.0, cb, xround, rank, C, gtid).x -
-                  mph * (double)cutmax_update<Elem, 3>(w, ke, be, kz, 3);
+        for (int i = 0; i < E; i += 2) {
+          const Elem y0 = cutmax_update<Elem, 3>(v[i], ke, be, kz, 3);
+          const Elem y1 = cutmax_update<Elem, 3>(v[i + 1], ke, be, kz, 3);
+          if (real(i)) ta += y0;
+          if (real(i + 1)) tb += y1;
         }
-        if (st == PAM_OK && !isfinite(total)) st = PAM_ERR_RANGE;
-        if (st == PAM_OK && normalize) {
-          if (!(total > 0.0)) {
-            st = PAM_ERR_RANGE;  // Z must be a distribution (pin A7)
-          } else if (rp.inv_mode == PAM_MODE_POLY) {
-            const pam_approx_config& ac = rp.inv;
-            const int rs = inv_rescaled(total, ac.iterations, ac.rescale, ac.scale_log2, ac.lo, ac.hi, &rnorm);
-            if (rs) st = rs;
-          } else {
-            rnorm = 1.0 / total;
-          }
+        const double tot = cluster_sum2<NTG>((double)ta + (double)tb, 0.0, cb, xround, rank, C, gtid).x -
+                           mph * (double)cutmax_update<Elem, 3>(w, ke, be, kz, 3);
+        if (warp == 0) {
+          double rn;
+          finish_total(tot, rn);
+          if (lane_of(gtid) == 0) cb->bc.re = rn;
         }
+        bar1();
+        re = (Elem)cb->bc.re;
       }
-      const Elem re = (Elem)rnorm;
       PAM_TRACE(tr, 22);
       if (merged) {
         if (dma) issue_upto(nch);  // small T: whatever the hooks did not issue yet
@@ -1083,13 +1171,25 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       xch_push<NTG, kArgmax>(nxt.x, nxt.y, best, besti, cb, xround, rank, C, gtid, [&]() {
         if (TMA) store_all(zr);
       });
-      const double2 rn = xch_wait<kArgmax>(best, besti, cb, xround, C, gtid);
-      PAM_TRACE(tr, 6 + 2 * (T - 1));
-      if (merged) {
-        S_in = rn.x;
-        Q_in = rn.y;
-        if (T == 1) R_in = cluster_sum2<NTG>(nxt.z, 0.0, cb, xround, rank, C, gtid).x;
+      if (merged && T == 1) {
+        // T = 1 needs the next input's third power sum too (one more exchange)
+        if (warp == 0) {
+          const double2 rn = xch_wait<kArgmax>(best, besti, cb, xround, C, gtid);
+          S_c = rn.x;
+          Q_c = rn.y;
+        } else {
+          ++xround;
+        }
+        const double r3 = cluster_sum2<NTG>(nxt.z, 0.0, cb, xround, rank, C, gtid).x;
+        if (warp == 0) R_c = r3;
+      } else if (warp == 0) {
+        const double2 rn = xch_wait<kArgmax>(best, besti, cb, xround, C, gtid);
+        S_c = rn.x;
+        Q_c = rn.y;
+      } else {
+        ++xround;
       }
+      PAM_TRACE(tr, 6 + 2 * (T - 1));
       in_ready = merged;
       k0_cur = k0next;
       if (rank == 0 && gtid == 0) {

@@ -16,20 +16,19 @@ CLK = 1.965e3  # cycles per us (SM clock under load)
 def names(T):  # p = 3 analytic-normaliser flow (the headline kernel)
     nm = {2: "input pass + xchg (1st row)", 4: "input moments"}
     for t in range(T - 1):
-        nm[13 + t] = f"chain {t}"
+        nm[13 + t] = f"control {t} (moments+chain, bcast)"
         nm[5 + 2 * t] = f"pass {t}" + (" (+3rd moment)" if t == T - 2 else "")
         nm[16 + t] = f"push {t} (bfly+barrier+send)"
-        nm[6 + 2 * t] = f"wait {t} (+record combine)"
-        nm[27 + t] = f"moments {t}"
-    nm.update({22: "chain + normaliser", 23: "X(next) wait", 24: "fused last pass + swap",
+        nm[6 + 2 * t] = f"wait {t} (warp 0: records)"
+    nm.update({22: "control + normaliser", 23: "X(next) wait", 24: "fused last pass + swap",
                6 + 2 * (T - 1): "closing xchg", 21: "status"})
     return nm
 
 
 def seq(T):
-    s = [0, 2, 4]
+    s = [0, 2]
     for t in range(T - 1):
-        s += [13 + t, 5 + 2 * t, 16 + t, 6 + 2 * t, 27 + t]
+        s += [13 + t, 5 + 2 * t, 16 + t, 6 + 2 * t]
     s += [22, 23, 24, 6 + 2 * (T - 1), 21]
     return s
 
