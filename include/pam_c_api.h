@@ -56,7 +56,8 @@ typedef enum pam_status {
   PAM_ERR_NON_FINITE = 5,       /* NonFiniteError: non-finite input row */
   PAM_ERR_CUDA = 6,             /* CUDA runtime error (launch / copy) */
   PAM_ERR_BAD_ARGUMENT = 7,     /* null pointer, bad shape or leading dimension */
-  PAM_ERR_UNSUPPORTED = 8       /* a parameter combination this build does not implement */
+  PAM_ERR_UNSUPPORTED = 8,      /* a parameter combination this build does not implement */
+  PAM_ERR_FORMAT = 9            /* FormatError          (errors.hpp:65): malformed logit file */
 } pam_status;
 
 /* Row flag bits OR-ed into the per-row status value's high byte (never an error). */
@@ -172,6 +173,24 @@ int pam_gumbel_sample_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int6
                                 int32_t* d_token, uint8_t* d_inside,
                                 double* d_onehot, int64_t ld_onehot,
                                 int32_t* d_row_status, void* stream);
+
+/* ---- logit files (csrc/ingest.cpp) -------------------------
+ * LGT1:  "LGT1" | u16 version (1) | u32 count | u32 n | count*n little-endian float32.
+ * JSONL: one JSON array of numbers per line, all of one length.
+ * Readers fill a caller buffer (pinned host memory feeds the batch API with one
+ * copy).  PAM_ERR_FORMAT sets info->err_offset (byte offset); PAM_ERR_NON_FINITE
+ * sets info->bad_vector (first vector with NaN/Inf; the data is still written).
+ * Replaces cli::ingest and the LogitFile writer. */
+typedef struct pam_ingest_info {
+  int64_t count, n;    /* vectors, length */
+  int64_t err_offset;  /* PAM_ERR_FORMAT: byte offset of the problem, else -1 */
+  int64_t bad_vector;  /* PAM_ERR_NON_FINITE: first non-finite vector, else -1 */
+} pam_ingest_info;
+int pam_lgt1_probe(const char* path, pam_ingest_info* info);
+int pam_lgt1_read(const char* path, float* dst, int64_t capacity, pam_ingest_info* info);
+int pam_lgt1_write(const char* path, const float* src, int64_t count, int64_t n);
+int pam_jsonl_probe(const char* path, pam_ingest_info* info);
+int pam_jsonl_read(const char* path, double* dst, int64_t capacity, pam_ingest_info* info);
 
 /* ---- introspection (bench / tests) --------------------------------------- */
 typedef struct pam_launch_info {

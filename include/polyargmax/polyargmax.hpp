@@ -122,7 +122,16 @@ void nucleus_sample_batch_device(const double* dX, std::size_t B, std::size_t n,
                                  const SamplerConfig& cfg, const CutMaxParams& params, std::int32_t* dToken,
                                  std::uint8_t* dInside, std::int32_t* dStatus, void* stream);
 
+// ---- logit files -----------------------------------------
+/// ingest: an LGT1 file (detected by its magic) or JSON lines.
+/// Throws FormatError(byte offset) / NonFiniteError(vector index).
+std::vector<LogitVector> ingest(const std::string& path);
+/// LGT1 writer: values are stored as float32; ingest(write(v)) == v bit-exact for
+/// float-representable inputs.
+void writeLgt1(const std::string& path, const std::vector<LogitVector>& vectors);
+
 /// Map a pam_status to the matching errors.hpp exception (no-op for PAM_OK).
-void throw_status(int status, std::size_t row = 0);
+/// `where` is the row / vector index, or the byte offset for PAM_ERR_FORMAT.
+void throw_status(int status, std::size_t where = 0);
 
 }  // namespace polyargmax

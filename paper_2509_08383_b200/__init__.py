@@ -2,19 +2,19 @@
 the Beta-cut nucleus sampler as hand-written sm_100a CUDA kernels behind a C ABI
 (include/pam_c_api.h) and the reference's `polyargmax` interface."""
 from . import _abi
-from .errors import (CudaError, DegenerateInputError, DomainError, Error, InvalidParamsError, NonFiniteError,
-                     RangeError)
+from .errors import (CudaError, DegenerateInputError, DomainError, Error, FormatError, InvalidParamsError,
+                     NonFiniteError, RangeError)
 from .polyargmax import (ApproxConfig, CutMaxParams, ResidualStats, SampleOutcome, SamplerConfig, ScoreVector,
                          betaInverseCdf, cutmax, cutmax_batch, cutmax_batch_device, cutmaxStep, goldschmidtInv,
                          goldschmidtInvSqrt, gumbel_sample_batch_device, gumbelFromUniform, gumbelMaxSample,
                          kernel_launch_count, launch_info, nucleus_sample_batch_device, nucleusAlpha,
-                         nucleusOneShotSample, uniform)
+                         nucleusOneShotSample, uniform, violationExperiment, ingest, ingest_pinned, write_lgt1)
 
 __all__ = [
     "ApproxConfig", "CutMaxParams", "ResidualStats", "SampleOutcome", "SamplerConfig", "ScoreVector",
     "betaInverseCdf", "cutmax", "cutmax_batch", "cutmax_batch_device", "cutmaxStep", "goldschmidtInv",
     "goldschmidtInvSqrt", "gumbel_sample_batch_device", "gumbelFromUniform", "gumbelMaxSample",
     "kernel_launch_count", "launch_info", "nucleus_sample_batch_device", "nucleusAlpha", "nucleusOneShotSample",
-    "uniform", "Error", "DegenerateInputError", "InvalidParamsError", "RangeError", "DomainError",
+    "uniform", "violationExperiment", "ingest", "ingest_pinned", "write_lgt1", "Error", "FormatError", "DegenerateInputError", "InvalidParamsError", "RangeError", "DomainError",
     "NonFiniteError", "CudaError",
 ]

@@ -20,6 +20,7 @@ PAM_ERR_NON_FINITE = 5
 PAM_ERR_CUDA = 6
 PAM_ERR_BAD_ARGUMENT = 7
 PAM_ERR_UNSUPPORTED = 8
+PAM_ERR_FORMAT = 9
 PAM_ROW_FLAG_TIE = 0x100
 
 PAM_RESCALE_AUTO, PAM_RESCALE_STATIC, PAM_RESCALE_NONE = 0, 1, 2
@@ -69,6 +70,10 @@ class pam_launch_info(C.Structure):
                  "groups")]
 
 
+class pam_ingest_info(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("count", "n", "err_offset", "bad_vector")]
+
+
 _P = C.c_void_p
 _I64 = C.c_int64
 
@@ -96,6 +101,11 @@ SIGNATURES = {
     "pam_kernel_launch_count": (C.c_int64, []),
     "pam_last_cuda_error": (C.c_char_p, []),
     "pam_set_trace_buffer": (None, [_P, _I64]),
+    "pam_lgt1_probe": (C.c_int, [C.c_char_p, C.POINTER(pam_ingest_info)]),
+    "pam_lgt1_read": (C.c_int, [C.c_char_p, _P, _I64, C.POINTER(pam_ingest_info)]),
+    "pam_lgt1_write": (C.c_int, [C.c_char_p, _P, _I64, _I64]),
+    "pam_jsonl_probe": (C.c_int, [C.c_char_p, C.POINTER(pam_ingest_info)]),
+    "pam_jsonl_read": (C.c_int, [C.c_char_p, _P, _I64, C.POINTER(pam_ingest_info)]),
 }
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))

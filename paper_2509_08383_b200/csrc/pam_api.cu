@@ -401,6 +401,7 @@ const char* pam_status_string(int status) {
     case PAM_ERR_CUDA: return "CUDA error";
     case PAM_ERR_BAD_ARGUMENT: return "bad argument";
     case PAM_ERR_UNSUPPORTED: return "unsupported";
+    case PAM_ERR_FORMAT: return "malformed logit file";
     default: return "unknown status";
   }
 }

@@ -42,8 +42,49 @@ void throw_status(int status, std::size_t row) {
     case PAM_ERR_NON_FINITE: throw NonFiniteError(msg, row);
     case PAM_ERR_UNSUPPORTED: throw InvalidParamsError(msg);
     case PAM_ERR_BAD_ARGUMENT: throw InvalidParamsError(msg);
+    case PAM_ERR_FORMAT: throw FormatError(msg, row);
     default: throw Error(msg + ": " + pam_last_cuda_error());
   }
+}
+
+std::vector<LogitVector> ingest(const std::string& path) {
+  pam_ingest_info info;
+  std::vector<LogitVector> out;
+  int st = pam_lgt1_probe(path.c_str(), &info);
+  if (st == PAM_OK) {
+    std::vector<float> buf((size_t)(info.count * info.n));
+    st = pam_lgt1_read(path.c_str(), buf.data(), (int64_t)buf.size(), &info);
+    if (st == PAM_ERR_NON_FINITE) throw_status(st, (std::size_t)info.bad_vector);
+    throw_status(st, (std::size_t)info.err_offset);
+    for (int64_t r = 0; r < info.count; ++r)
+      out.emplace_back(buf.begin() + r * info.n, buf.begin() + (r + 1) * info.n);
+    return out;
+  }
+  if (st == PAM_ERR_FORMAT && info.err_offset == 0) {  // not LGT1 at all: JSON lines
+    st = pam_jsonl_probe(path.c_str(), &info);
+    if (st == PAM_OK) {
+      std::vector<double> buf((size_t)(info.count * info.n));
+      st = pam_jsonl_read(path.c_str(), buf.data(), (int64_t)buf.size(), &info);
+      if (st == PAM_ERR_NON_FINITE) throw_status(st, (std::size_t)info.bad_vector);
+      throw_status(st, 0);
+      for (int64_t r = 0; r < info.count; ++r)
+        out.emplace_back(buf.begin() + r * info.n, buf.begin() + (r + 1) * info.n);
+      return out;
+    }
+  }
+  throw_status(st, st == PAM_ERR_FORMAT ? (std::size_t)info.err_offset : 0);
+  return out;
+}
+
+void writeLgt1(const std::string& path, const std::vector<LogitVector>& vectors) {
+  const std::size_t n = vectors.empty() ? 0 : vectors[0].size();
+  std::vector<float> buf;
+  buf.reserve(vectors.size() * n);
+  for (const auto& v : vectors) {
+    if (v.size() != n) throw InvalidParamsError("writeLgt1: vectors of different lengths");
+    for (double x : v) buf.push_back((float)x);
+  }
+  throw_status(pam_lgt1_write(path.c_str(), buf.data(), (int64_t)vectors.size(), (int64_t)n));
 }
 
 ApproxConfig ApproxConfig::invsqrtPreset(int alphaBits) {

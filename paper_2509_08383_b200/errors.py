@@ -33,6 +33,14 @@ class NonFiniteError(Error):
         self.vector_index = vector_index
 
 
+class FormatError(Error):
+    """Malformed logit file; carries the byte offset of the problem (errors.hpp:65)."""
+
+    def __init__(self, msg: str, byte_offset: int):
+        super().__init__(f"{msg} (byte offset {byte_offset})")
+        self.byte_offset = byte_offset
+
+
 class CudaError(Error):
     """CUDA launch or copy failure inside the library."""
 
@@ -59,6 +67,8 @@ def raise_for_status(status: int, row: int = 0, what: str = "") -> None:
         msg = f"{what}: {msg}"
     if s == _abi.PAM_ERR_NON_FINITE:
         raise NonFiniteError(msg, row)
+    if s == _abi.PAM_ERR_FORMAT:
+        raise FormatError(msg, row)
     if s == _abi.PAM_ERR_CUDA:
         msg += ": " + lib.pam_last_cuda_error().decode()
     cls = _BY_STATUS.get(s, Error)

@@ -20,6 +20,7 @@ computes on the CPU except argument marshalling.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence, Union
 
@@ -355,6 +356,81 @@ def gumbelMaxSample(x, params: Optional[CutMaxParams] = None, seed: int = 0, nuc
     """gumbelMaxSample (SPEC.md:407-415)."""
     return _one_row_sample(gumbel_sample_batch_device, x, SamplerConfig(p=nucleus_p, seed=seed),
                            params or CutMaxParams(), 0)
+
+
+# ---- logit files (SPEC.md:530-551; csrc/ingest.cpp) --------------------------------
+def _read_file(path: str, pinned: bool):
+    info = _abi.pam_ingest_info()
+    bpath = os.fsencode(path)
+    st = _lib.pam_lgt1_probe(bpath, C.byref(info))
+    kind, dtype = "lgt1", np.float32
+    if st == _abi.PAM_ERR_FORMAT and info.err_offset == 0:  # no LGT1 magic: JSON lines
+        st = _lib.pam_jsonl_probe(bpath, C.byref(info))
+        kind, dtype = "jsonl", np.float64
+    raise_for_status(st, row=info.err_offset, what=f"ingest {path}")
+    shape = (int(info.count), int(info.n))
+    if pinned:
+        torch = _torch()
+        buf = torch.empty(shape, dtype=torch.float32 if dtype == np.float32 else torch.float64, pin_memory=True)
+        ptr = buf.data_ptr()
+    else:
+        buf = np.empty(shape, dtype=dtype)
+        ptr = buf.ctypes.data
+    fn = _lib.pam_lgt1_read if kind == "lgt1" else _lib.pam_jsonl_read
+    st = fn(bpath, ptr, shape[0] * shape[1], C.byref(info))
+    raise_for_status(st, row=info.bad_vector if st == _abi.PAM_ERR_NON_FINITE else info.err_offset,
+                     what=f"ingest {path}")
+    return buf
+
+
+def ingest(path: str) -> np.ndarray:
+    """ingest: an LGT1 file (float32 [count, n]) or JSON lines
+    (float64 [count, n]).  Raises FormatError (byte offset) / NonFiniteError (vector)."""
+    return _read_file(path, pinned=False)
+
+
+def ingest_pinned(path: str):
+    """ingest straight into pinned host memory (a torch tensor) so the batch API
+    can take it to the GPU with one async copy: ingest_pinned(p).cuda(non_blocking=True)."""
+    return _read_file(path, pinned=True)
+
+
+def write_lgt1(path: str, vectors) -> None:
+    """LGT1 writer; ingest(write_lgt1(v)) == float32(v) bit-exact."""
+    a = np.ascontiguousarray(np.asarray(vectors, dtype=np.float32))
+    if a.ndim != 2:
+        raise InvalidParamsError("write_lgt1 expects a 2-D array [count, n]")
+    raise_for_status(_lib.pam_lgt1_write(os.fsencode(path), a.ctypes.data, a.shape[0], a.shape[1]))
+
+
+def violationExperiment(prompts, cfg: SamplerConfig, draws: int, params: Optional[CutMaxParams] = None) -> dict:
+    """violationExperiment (§4.3 / Fig. 4) on the GPU
+    samplers.  For every prompt, `draws` independent samples (noise keyed by
+    (seed ^ prompt) ^ draw-row) from the Beta-cut sampler and from Gumbel-max;
+    a violation is a token outside the plaintext top-p nucleus.
+    Returns per-method (mean, std) of the per-prompt violation fractions and
+    the per-prompt arrays.  Deterministic under a fixed seed."""
+    torch = _torch()
+    if draws < 1:
+        raise InvalidParamsError("draws must be >= 1")  # SPEC.md:454
+    params = params or CutMaxParams()
+    rates = {"betaCut": [], "gumbel": []}
+    for i, x in enumerate(prompts):
+        xv = torch.as_tensor(np.asarray(x, dtype=np.float64), device="cuda")
+        X = xv[None, :].repeat(draws, 1)
+        c = SamplerConfig(p=cfg.p, q=cfg.q, alpha=cfg.alpha, seed=cfg.seed ^ i, draw=cfg.draw)
+        for name, fn in (("betaCut", nucleus_sample_batch_device), ("gumbel", gumbel_sample_batch_device)):
+            _, inside, st = fn(X, c, params)
+            st_h = st.cpu().numpy()
+            if np.any(st_h != 0):
+                raise_for_status(int(st_h[st_h != 0][0]), row=int(np.nonzero(st_h)[0][0]))
+            rates[name].append(1.0 - float(inside.double().mean().item()))
+    out = {}
+    for name, r in rates.items():
+        a = np.asarray(r)
+        out[name + "Rate"] = (float(a.mean()), float(a.std()))
+        out[name + "PerPrompt"] = a
+    return out
 
 
 def cutmaxStep(y, p: int, c: float, epsVar: float = 1e-24):

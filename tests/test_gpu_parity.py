@@ -372,3 +372,24 @@ def test_launch_count_and_native_library(cuda, pam):
     assert pam.kernel_launch_count() == before + 1
     info = pam.launch_info(8, 4096, 151936)
     assert info["cluster"] >= 2 and info["clusters"] > 0
+
+
+def test_violation_experiment_gpu(cuda, pam, orc):
+    """§8(f) rank 1 (§4.3 / Fig. 4) on the GPU samplers:
+    peaked logits, p = 0.9 -> Beta-cut violation rate 0, Gumbel-max > 0; the
+    GPU outcomes equal the oracle's draw for draw on two prompts."""
+    rng = np.random.default_rng(16)
+    prompts = [rng.permutation(-1.1 * np.log(np.arange(1, 2049)) + rng.normal(0, 0.3, 2048)) for _ in range(20)]
+    cfg = pam.SamplerConfig(p=0.9, seed=1234)
+    out = pam.violationExperiment(prompts, cfg, draws=200)
+    assert out["betaCutRate"][0] == 0.0
+    assert out["gumbelRate"][0] > 0.0
+    for i in (0, 7):
+        X = np.repeat(np.asarray(prompts[i])[None, :], 200, axis=0)
+        c = pam.SamplerConfig(p=0.9, seed=1234 ^ i).lower()
+        _, ins_b, _ = orc.sample_batch(X, c, pam.CutMaxParams().lower())
+        _, ins_g, _ = orc.sample_batch(X, c, pam.CutMaxParams().lower(), gumbel=True)
+        assert 1.0 - ins_b.mean() == out["betaCutPerPrompt"][i]
+        assert abs((1.0 - ins_g.mean()) - out["gumbelPerPrompt"][i]) < 1e-12
+    with pytest.raises(pam.InvalidParamsError):
+        pam.violationExperiment(prompts[:1], cfg, draws=0)
