@@ -19,6 +19,7 @@
 
 #include <stdint.h>
 #include <math.h>
+#include <string.h>
 
 #if defined(__CUDACC__)
 #define PAM_HD __host__ __device__ __forceinline__
@@ -174,6 +175,30 @@ PAM_HD double uniform_at(uint64_t seed, uint64_t row, uint64_t draw, uint64_t i)
 }
 
 // ------------------------------------------------------- exp / log -------
+// Exponent-field helpers: exact replacements for ldexp / frexp on the normal
+// range (scaling by 2^k is exact there, so results are bit-identical to the
+// library calls the oracle uses); the library calls remain for subnormals.
+PAM_HD double pam_bits_to_double(uint64_t b) {
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)b);
+#else
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+#endif
+}
+PAM_HD uint64_t pam_double_to_bits(double d) {
+#ifdef __CUDA_ARCH__
+  return (uint64_t)__double_as_longlong(d);
+#else
+  uint64_t b;
+  memcpy(&b, &d, 8);
+  return b;
+#endif
+}
+// 2^k for -1022 <= k <= 1023
+PAM_HD double pam_pow2(int k) { return pam_bits_to_double((uint64_t)(k + 1023) << 52); }
+
 // exp: x = k ln2 + r, |r| <= ln2/2, degree-13 Taylor (Horner, fma).  Results
 // below 2^-1022 are flushed to +0 (pinned, keeps both sides identical).
 PAM_HD double exp_p(double x) {
@@ -205,7 +230,8 @@ PAM_HD double exp_p(double x) {
     const double t = ldexp(p, ki + 60);
     return (t < 0x1p-962) ? 0.0 : ldexp(t, -60);
   }
-  return ldexp(p, ki);
+  if (ki > 1023) return (p * pam_pow2(ki - 1)) * 2.0;  // ki = 1024 (x near the overflow bound)
+  return p * pam_pow2(ki);                             // == ldexp(p, ki): exact scaling
 }
 
 // log: x = 2^e m, m in [sqrt(1/2), sqrt(2)), f = (m-1)/(m+1),
@@ -216,7 +242,14 @@ PAM_HD double log_p(double x) {
   if (x == 0.0) return -HUGE_VAL;
   if (x > 1.79769313486231570815e308) return x;  // +inf
   int e;
-  double m = frexp(x, &e);
+  double m;
+  const uint64_t xb = pam_double_to_bits(x);
+  if ((xb >> 52) != 0) {  // normal: == frexp(x, &e), m in [1/2, 1)
+    e = (int)(xb >> 52) - 1022;
+    m = pam_bits_to_double((xb & 0x000fffffffffffffULL) | 0x3fe0000000000000ULL);
+  } else {
+    m = frexp(x, &e);
+  }
   if (m < 0x1.6a09e667f3bcdp-1) { m = m + m; e = e - 1; }
   const double f = (m - 1.0) / (m + 1.0);
   const double s = f * f;

@@ -100,6 +100,15 @@ def test_host_scalars_match_oracle_bit_for_bit(pam, orc):
     for u in rng.uniform(0, 1, 500):
         assert pam.betaInverseCdf(u, 21.854345326782838) == orc.scalar("beta_icdf", u, 21.854345326782838)
         assert pam.gumbelFromUniform(u) == orc.scalar("gumbel", u)
+    # exp/log edge ranges through u^(1/alpha): deep underflow / subnormal flush
+    # (large 1/alpha), results near 1 (u -> 1), tiny u (2^-53)
+    us = np.concatenate([rng.uniform(0, 1, 300), 2.0 ** -rng.uniform(0, 53, 300), 1 - 2.0 ** -rng.uniform(1, 52, 100)])
+    for alpha in (0.0015, 0.01, 0.37, 58.40397509653449):
+        for u in us:
+            a, b = pam.betaInverseCdf(u, alpha), orc.scalar("beta_icdf", u, alpha)
+            assert a == b, (u, alpha, a, b)
+    for u in us:
+        assert pam.gumbelFromUniform(u) == orc.scalar("gumbel", u)
     for i in range(300):
         assert pam.uniform(2**63 + 5, 17, 3, i) == orc.scalar("uniform", 2**63 + 5, 17, 3, i)
     assert pam.nucleusAlpha(0.9) == orc.scalar("nucleus_alpha", 0.9, 0.9)
