@@ -57,7 +57,8 @@ typedef enum pam_status {
   PAM_ERR_CUDA = 6,             /* CUDA runtime error (launch / copy) */
   PAM_ERR_BAD_ARGUMENT = 7,     /* null pointer, bad shape or leading dimension */
   PAM_ERR_UNSUPPORTED = 8,      /* a parameter combination this build does not implement */
-  PAM_ERR_FORMAT = 9            /* FormatError          (errors.hpp:65): malformed logit file */
+  PAM_ERR_FORMAT = 9,           /* FormatError          (errors.hpp:65): malformed logit file */
+  PAM_ERR_SINGULAR = 10         /* SingularityError     (errors.hpp:55): JVP through s^2 < eps_var */
 } pam_status;
 
 /* Row flag bits OR-ed into the per-row status value's high byte (never an error). */
@@ -173,6 +174,22 @@ int pam_gumbel_sample_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int6
                                 int32_t* d_token, uint8_t* d_inside,
                                 double* d_onehot, int64_t ld_onehot,
                                 int32_t* d_row_status, void* stream);
+
+/* ---- analysis outputs (csrc/analysis_kernel.cuh) -------------------
+ * convergenceTrace: d_out[B][T][4] = {mu, s2, U, fraction of
+ * entries below the mean} per iteration, U = sum_{j != top} (r_j - rbar)^2 the
+ * non-top dispersion.  Entries after a failing iteration are
+ * not written; the row status says why.  Replaces core::convergenceTrace. */
+int pam_convergence_trace_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int64_t n,
+                                    const pam_cutmax_params* prm, double* d_out, int32_t* d_row_status,
+                                    void* stream);
+/* cutmaxJvp: d_dz = d cutmax(x; params) / dx . v, forward mode
+ * through mean, variance, 1/sqrt, odd power and normalisation; d_z (nullable) =
+ * cutmax(x).  x and v share ld_x.  s2 < eps_var -> PAM_ERR_SINGULAR per row.
+ * Replaces grad::cutmaxJvp (cutmaxJacobian = n JVPs, one batched call). */
+int pam_cutmax_jvp_batch_f64(const double* d_x, const double* d_v, int64_t ld_x, int64_t B, int64_t n,
+                             const pam_cutmax_params* prm, double* d_z, double* d_dz, int64_t ld_z,
+                             int32_t* d_row_status, void* stream);
 
 /* ---- logit files (csrc/ingest.cpp) -------------------------
  * LGT1:  "LGT1" | u16 version (1) | u32 count | u32 n | count*n little-endian float32.

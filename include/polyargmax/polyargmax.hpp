@@ -122,6 +122,20 @@ void nucleus_sample_batch_device(const double* dX, std::size_t B, std::size_t n,
                                  const SamplerConfig& cfg, const CutMaxParams& params, std::int32_t* dToken,
                                  std::uint8_t* dInside, std::int32_t* dStatus, void* stream);
 
+// ---- analysis ---------------------------------------------------
+/// One convergenceTrace entry: mu, s2, the non-top dispersion U
+/// and the fraction of entries below the mean (Fig. 3).
+struct TraceStep {
+  double mu = 0.0, s2 = 0.0, dispersion = 0.0, fractionBelowMean = 0.0;
+};
+std::vector<TraceStep> convergenceTrace(const LogitVector& x, const CutMaxParams& params);
+/// cutmaxJvp: forward-mode d cutmax(x)/dx . v on the GPU.
+/// Throws SingularityError if s2 < epsVar anywhere on the path.
+std::vector<double> cutmaxJvp(const LogitVector& x, const std::vector<double>& v, const CutMaxParams& params);
+/// cutmaxJacobian: n JVPs with the basis directions, one batched launch.
+/// Row-major n x n, J[i][j] = dZ_i / dx_j.
+std::vector<double> cutmaxJacobian(const LogitVector& x, const CutMaxParams& params);
+
 // ---- logit files -----------------------------------------
 /// ingest: an LGT1 file (detected by its magic) or JSON lines.
 /// Throws FormatError(byte offset) / NonFiniteError(vector index).

@@ -488,6 +488,68 @@ int orc_convergence_trace(const double* x, int64_t n, const pam_cutmax_params* p
   return st;
 }
 
+/* cutmaxJvp (§3.4): directional derivative of
+ * cutmax at x in direction v by forward-mode dual arithmetic through the mean,
+ * the population variance, 1/sqrt, the odd power and the normalisation:
+ *   mu' = mean(y'),  s2' = 2 mean((y - mu) y'),  k = 1/(c sqrt(s2)),
+ *   k' = -k s2' / (2 s2),  u = k (y - mu) + 1,  u' = k' (y - mu) + k (y' - mu'),
+ *   y_next = u^p,  y_next' = p u^(p-1) u',
+ *   Z = Y / S,  Z' = Y'/S - Y S'/S^2  (S = sum Y, S' = sum Y').
+ * s2 < eps_var anywhere on the path is the SingularityError (errors.hpp:55). */
+int orc_cutmax_jvp(const double* x, const double* v, int64_t n, const pam_cutmax_params* prm, double* z,
+                   double* dz) {
+  int st = orc_validate(prm, n);
+  if (st) return st;
+  if (prm->eps_stop > 0.0) return PAM_ERR_UNSUPPORTED;
+  double* y = (double*)malloc(sizeof(double) * (size_t)n);
+  double* dy = (double*)malloc(sizeof(double) * (size_t)n);
+  int64_t i;
+  int t;
+  for (i = 0; i < n; ++i) {
+    if (!isfinite(x[i]) || !isfinite(v[i])) { free(y); free(dy); return PAM_ERR_NON_FINITE; }
+    y[i] = x[i];
+    dy[i] = v[i];
+  }
+  for (t = 0; t < prm->T && st == PAM_OK; ++t) {
+    double sum = 0.0, dsum = 0.0;
+    for (i = 0; i < n; ++i) { sum += y[i]; dsum += dy[i]; }
+    const double mu = sum / (double)n, dmu = dsum / (double)n;
+    double ss = 0.0, dss = 0.0;
+    for (i = 0; i < n; ++i) {
+      const double d = y[i] - mu;
+      ss += d * d;
+      dss += d * dy[i];
+    }
+    const double s2 = ss / (double)n, ds2 = 2.0 * dss / (double)n;
+    if (!(s2 >= prm->eps_var)) { st = PAM_ERR_SINGULAR; break; }
+    const double k = (1.0 / sqrt(s2)) * (1.0 / prm->c[t]);
+    const double dk = -k * ds2 / (2.0 * s2);
+    const int p = prm->p[t];
+    for (i = 0; i < n; ++i) {
+      const double d = y[i] - mu;
+      const double u = d * k + 1.0;
+      const double du = dk * d + k * (dy[i] - dmu);
+      y[i] = orc_ipow(u, p);
+      dy[i] = (double)p * orc_ipow(u, p - 1) * du;
+    }
+  }
+  if (st == PAM_OK) {
+    double S = 0.0, dS = 0.0;
+    for (i = 0; i < n; ++i) { S += y[i]; dS += dy[i]; }
+    if (!(S > 0.0) || !isfinite(S)) st = PAM_ERR_RANGE;
+    else {
+      const double r = 1.0 / S;
+      for (i = 0; i < n; ++i) {
+        if (z) z[i] = y[i] * r;
+        dz[i] = dy[i] * r - y[i] * dS * r * r;
+      }
+    }
+  }
+  free(y);
+  free(dy);
+  return st;
+}
+
 /* ---------------------------------------------------------- sampling ----- */
 
 /* Nucleus membership ground truth (top-p definition):

@@ -78,6 +78,8 @@ int orc_fixed_point_target(int64_t n, int p, double c, double* out /* n */, doub
 int orc_contraction_factor(int64_t n, int p, double c, double* kappa);
 /* convergenceTrace: per iteration {mu, s2, dispersion, frac_below_mean} */
 int orc_convergence_trace(const double* x, int64_t n, const pam_cutmax_params* prm, double* out /* T x 4 */);
+/* cutmaxJvp: forward-mode directional derivative (and Z) */
+int orc_cutmax_jvp(const double* x, const double* v, int64_t n, const pam_cutmax_params* prm, double* z, double* dz);
 
 /* TieWarning flag: PAM_ROW_FLAG_TIE if the input top-2 gap < 1e-9, else 0 */
 int orc_tie_warning(const double* x, int64_t n);

@@ -41,6 +41,7 @@ _SIG = {
     "orc_fixed_point_target": (C.c_int, [_I64, C.c_int, C.c_double, _P, _P]),
     "orc_contraction_factor": (C.c_int, [_I64, C.c_int, C.c_double, _P]),
     "orc_convergence_trace": (C.c_int, [_P, _I64, _PRM, _P]),
+    "orc_cutmax_jvp": (C.c_int, [_P, _P, _I64, _PRM, _P, _P]),
     "orc_tie_warning": (C.c_int, [_P, _I64]),
     "orc_nucleus_inside": (C.c_int, [_P, _I64, C.c_double, _I64]),
     "orc_sample": (C.c_int, [_P, _I64, C.POINTER(_abi.pam_sampler_cfg), _PRM, C.c_uint64, C.c_int, _P, _P, _P]),
@@ -152,6 +153,16 @@ def convergence_trace(x, prm):
     out = np.zeros((prm.T, 4))
     st = load().orc_convergence_trace(x.ctypes.data, x.shape[0], C.byref(prm), out.ctypes.data)
     return st, out
+
+
+def cutmax_jvp(x, v, prm):
+    """-> (status, z, dz): forward-mode JVP of cutmax at x in direction v."""
+    x = _f64(x)
+    v = _f64(v)
+    z = np.empty_like(x)
+    dz = np.empty_like(x)
+    st = load().orc_cutmax_jvp(x.ctypes.data, v.ctypes.data, x.shape[0], C.byref(prm), z.ctypes.data, dz.ctypes.data)
+    return st, z, dz
 
 
 def tie_warning(x) -> int:

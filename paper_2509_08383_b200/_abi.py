@@ -21,6 +21,7 @@ PAM_ERR_CUDA = 6
 PAM_ERR_BAD_ARGUMENT = 7
 PAM_ERR_UNSUPPORTED = 8
 PAM_ERR_FORMAT = 9
+PAM_ERR_SINGULAR = 10
 PAM_ROW_FLAG_TIE = 0x100
 
 PAM_RESCALE_AUTO, PAM_RESCALE_STATIC, PAM_RESCALE_NONE = 0, 1, 2
@@ -101,6 +102,9 @@ SIGNATURES = {
     "pam_kernel_launch_count": (C.c_int64, []),
     "pam_last_cuda_error": (C.c_char_p, []),
     "pam_set_trace_buffer": (None, [_P, _I64]),
+    "pam_convergence_trace_batch_f64": (C.c_int, [_P, _I64, _I64, _I64, C.POINTER(pam_cutmax_params), _P, _P, _P]),
+    "pam_cutmax_jvp_batch_f64": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(pam_cutmax_params), _P, _P, _I64,
+                                           _P, _P]),
     "pam_lgt1_probe": (C.c_int, [C.c_char_p, C.POINTER(pam_ingest_info)]),
     "pam_lgt1_read": (C.c_int, [C.c_char_p, _P, _I64, C.POINTER(pam_ingest_info)]),
     "pam_lgt1_write": (C.c_int, [C.c_char_p, _P, _I64, _I64]),

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/pam_c_api.h"
+#include "analysis_kernel.cuh"
 #include "cutmax_kernel.cuh"
 #include "nucleus_kernel.cuh"
 #include "pam_variants.h"
@@ -309,6 +310,55 @@ int sampler_batch_impl(const double* d_x, int64_t ld_x, int64_t B, int64_t n, co
   return launch_cluster_kernel(fn, var->nt, C, clusters, smem, stream, &sa);
 }
 
+// ---------------------------------------------------- analysis kernels (§8f)
+// Smallest cluster whose CTAs hold ceil(n/C) in registers with one of the
+// analysis variants; rows stream over min(B, active clusters) clusters.
+int analysis_impl(bool jvp, const double* d_x, const double* d_v, int64_t ld_x, int64_t B, int64_t n,
+                  const pam_cutmax_params* prm, double* d_z, double* d_dz, int64_t ld_z, double* d_out,
+                  int32_t* d_status, cudaStream_t stream) {
+  if (!prm) return PAM_ERR_BAD_ARGUMENT;
+  int st = pam_validate_cutmax_params(prm, n);
+  if (st) return st;
+  if (prm->eps_stop > 0.0) return PAM_ERR_UNSUPPORTED;
+  if (B < 0 || ld_x < n || (B > 0 && !d_x)) return PAM_ERR_BAD_ARGUMENT;
+  if (jvp && B > 0 && (!d_v || !d_dz || ld_z < n)) return PAM_ERR_BAD_ARGUMENT;
+  if (B == 0) return PAM_OK;
+  const AnalysisVariant* var = nullptr;
+  int C = 0;
+  int64_t L = 0;
+  for (int c = 1; c <= 16 && !var; ++c) {
+    L = (n + c - 1) / c;
+    for (int i = 0; i < kNumAnalysisVariants; ++i) {
+      const AnalysisVariant& v = kAnalysisVariants[i];
+      if ((int64_t)v.nt * v.e >= L && (!var || v.nt * v.e < var->nt * var->e)) var = &v;
+    }
+    if (var) C = c;
+  }
+  if (!var) return PAM_ERR_UNSUPPORTED;
+  const void* fn = jvp ? var->jvp : var->trace;
+  const int smem = (int)sizeof(ControlBlock);
+  const int maxcl = max_active_clusters(fn, var->nt, C, smem);
+  if (maxcl <= 0) return cuda_fail(cudaErrorInvalidConfiguration, "no cluster fits (occupancy 0)");
+  const int clusters = (int)(B < maxcl ? B : maxcl);
+  AnalysisArgs aa;
+  memset(&aa, 0, sizeof aa);
+  aa.x = d_x;
+  aa.v = d_v;
+  aa.z = d_z;
+  aa.dz = d_dz;
+  aa.out = d_out;
+  aa.status = d_status;
+  aa.ldx = ld_x;
+  aa.ldz = ld_z;
+  aa.B = B;
+  aa.n = n;
+  aa.L = (int32_t)L;
+  aa.ctrl_offset = 0;
+  aa.inv_n = 1.0 / (double)n;
+  fill_row_params(prm, &aa.rp);
+  return launch_cluster_kernel(fn, var->nt, C, clusters, smem, stream, &aa);
+}
+
 // ---------------------------------------------------- host-buffer e2e path
 struct HostWorkspace {
   std::mutex mu;
@@ -402,6 +452,7 @@ const char* pam_status_string(int status) {
     case PAM_ERR_BAD_ARGUMENT: return "bad argument";
     case PAM_ERR_UNSUPPORTED: return "unsupported";
     case PAM_ERR_FORMAT: return "malformed logit file";
+    case PAM_ERR_SINGULAR: return "singular (variance below eps_var on the JVP path)";
     default: return "unknown status";
   }
 }
@@ -523,6 +574,21 @@ int pam_gumbel_sample_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int6
                                 int64_t ld_onehot, int32_t* d_row_status, void* stream) {
   return sampler_batch_impl(d_x, ld_x, B, n, cfg, prm, d_token, d_inside, d_onehot, ld_onehot, d_row_status,
                             (cudaStream_t)stream, true);
+}
+
+int pam_convergence_trace_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int64_t n,
+                                    const pam_cutmax_params* prm, double* d_out, int32_t* d_row_status,
+                                    void* stream) {
+  if (B > 0 && !d_out) return PAM_ERR_BAD_ARGUMENT;
+  return analysis_impl(false, d_x, nullptr, ld_x, B, n, prm, nullptr, nullptr, n, d_out, d_row_status,
+                       (cudaStream_t)stream);
+}
+
+int pam_cutmax_jvp_batch_f64(const double* d_x, const double* d_v, int64_t ld_x, int64_t B, int64_t n,
+                             const pam_cutmax_params* prm, double* d_z, double* d_dz, int64_t ld_z,
+                             int32_t* d_row_status, void* stream) {
+  return analysis_impl(true, d_x, d_v, ld_x, B, n, prm, d_z, d_dz, ld_z, nullptr, d_row_status,
+                       (cudaStream_t)stream);
 }
 
 int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_params* prm, pam_launch_info* info) {

@@ -10,6 +10,13 @@ struct Variant {
   const void* fn[2];          // [P==3]
 };
 
+// Analysis kernels (analysis_kernel.cuh): convergence trace and forward-mode JVP.
+struct AnalysisVariant {
+  int nt, e;
+  const void* trace;
+  const void* jvp;
+};
+
 struct SamplerVariant {
   int nt, e;
   const void* fn[2][2];  // [P==3][GUMBEL]
@@ -17,6 +24,8 @@ struct SamplerVariant {
 
 extern const Variant kCutmaxVariants[];
 extern const int kNumCutmaxVariants;
+extern const AnalysisVariant kAnalysisVariants[];
+extern const int kNumAnalysisVariants;
 extern const SamplerVariant kSamplerVariants[];
 extern const int kNumSamplerVariants;
 

@@ -43,6 +43,7 @@ void throw_status(int status, std::size_t row) {
     case PAM_ERR_UNSUPPORTED: throw InvalidParamsError(msg);
     case PAM_ERR_BAD_ARGUMENT: throw InvalidParamsError(msg);
     case PAM_ERR_FORMAT: throw FormatError(msg, row);
+    case PAM_ERR_SINGULAR: throw SingularityError(msg + " (row " + std::to_string(row) + ")");
     default: throw Error(msg + ": " + pam_last_cuda_error());
   }
 }
@@ -74,6 +75,62 @@ std::vector<LogitVector> ingest(const std::string& path) {
   }
   throw_status(st, st == PAM_ERR_FORMAT ? (std::size_t)info.err_offset : 0);
   return out;
+}
+
+namespace {
+using DevBuf = DeviceBuffer;
+// JVPs of B directions (row-major B x n) at x; returns dZ row-major B x n
+std::vector<double> jvp_rows(const LogitVector& x, const std::vector<double>& V, std::size_t B,
+                             const CutMaxParams& params) {
+  const std::size_t n = x.size();
+  const pam_cutmax_params prm = params.lower();
+  DevBuf dx(B * n * 8), dv(B * n * 8), ddz(B * n * 8), dst(B * 4);
+  for (std::size_t r = 0; r < B; ++r)
+    check_cuda(cudaMemcpy((double*)dx.p + r * n, x.data(), n * 8, cudaMemcpyHostToDevice), "H2D");
+  check_cuda(cudaMemcpy(dv.p, V.data(), B * n * 8, cudaMemcpyHostToDevice), "H2D");
+  throw_status(pam_cutmax_jvp_batch_f64((const double*)dx.p, (const double*)dv.p, (int64_t)n, (int64_t)B,
+                                        (int64_t)n, &prm, nullptr, (double*)ddz.p, (int64_t)n, (int32_t*)dst.p,
+                                        nullptr));
+  std::vector<double> dz(B * n);
+  std::vector<int32_t> st(B);
+  check_cuda(cudaMemcpy(dz.data(), ddz.p, B * n * 8, cudaMemcpyDeviceToHost), "D2H");
+  check_cuda(cudaMemcpy(st.data(), dst.p, B * 4, cudaMemcpyDeviceToHost), "D2H");
+  for (std::size_t r = 0; r < B; ++r) throw_status(st[r], r);
+  return dz;
+}
+}  // namespace
+
+std::vector<TraceStep> convergenceTrace(const LogitVector& x, const CutMaxParams& params) {
+  const std::size_t n = x.size();
+  const pam_cutmax_params prm = params.lower();
+  DevBuf dx(n * 8), dout((std::size_t)prm.T * 4 * 8), dst(4);
+  check_cuda(cudaMemcpy(dx.p, x.data(), n * 8, cudaMemcpyHostToDevice), "H2D");
+  throw_status(pam_convergence_trace_batch_f64((const double*)dx.p, (int64_t)n, 1, (int64_t)n, &prm,
+                                               (double*)dout.p, (int32_t*)dst.p, nullptr));
+  std::vector<double> out((std::size_t)prm.T * 4);
+  int32_t st = 0;
+  check_cuda(cudaMemcpy(out.data(), dout.p, out.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  check_cuda(cudaMemcpy(&st, dst.p, 4, cudaMemcpyDeviceToHost), "D2H");
+  throw_status(st);
+  std::vector<TraceStep> steps((std::size_t)prm.T);
+  for (int t = 0; t < prm.T; ++t) steps[t] = {out[4 * t], out[4 * t + 1], out[4 * t + 2], out[4 * t + 3]};
+  return steps;
+}
+
+std::vector<double> cutmaxJvp(const LogitVector& x, const std::vector<double>& v, const CutMaxParams& params) {
+  if (v.size() != x.size()) throw InvalidParamsError("cutmaxJvp: v and x differ in length");
+  return jvp_rows(x, v, 1, params);
+}
+
+std::vector<double> cutmaxJacobian(const LogitVector& x, const CutMaxParams& params) {
+  const std::size_t n = x.size();
+  std::vector<double> I(n * n, 0.0);
+  for (std::size_t j = 0; j < n; ++j) I[j * n + j] = 1.0;
+  const std::vector<double> cols = jvp_rows(x, I, n, params);  // row j = J e_j (column j of J)
+  std::vector<double> J(n * n);
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j = 0; j < n; ++j) J[i * n + j] = cols[j * n + i];
+  return J;
 }
 
 void writeLgt1(const std::string& path, const std::vector<LogitVector>& vectors) {

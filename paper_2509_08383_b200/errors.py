@@ -41,6 +41,10 @@ class FormatError(Error):
         self.byte_offset = byte_offset
 
 
+class SingularityError(Error):
+    """Variance below eps_var on the JVP path (errors.hpp:55)."""
+
+
 class CudaError(Error):
     """CUDA launch or copy failure inside the library."""
 
@@ -53,6 +57,7 @@ _BY_STATUS = {
     _abi.PAM_ERR_CUDA: CudaError,
     _abi.PAM_ERR_BAD_ARGUMENT: InvalidParamsError,
     _abi.PAM_ERR_UNSUPPORTED: InvalidParamsError,
+    _abi.PAM_ERR_SINGULAR: SingularityError,
 }
 
 
@@ -72,6 +77,6 @@ def raise_for_status(status: int, row: int = 0, what: str = "") -> None:
     if s == _abi.PAM_ERR_CUDA:
         msg += ": " + lib.pam_last_cuda_error().decode()
     cls = _BY_STATUS.get(s, Error)
-    if s in (_abi.PAM_ERR_DEGENERATE_INPUT, _abi.PAM_ERR_RANGE):
+    if s in (_abi.PAM_ERR_DEGENERATE_INPUT, _abi.PAM_ERR_RANGE, _abi.PAM_ERR_SINGULAR):
         msg += f" (row {row})"
     raise cls(msg)

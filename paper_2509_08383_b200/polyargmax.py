@@ -358,6 +358,87 @@ def gumbelMaxSample(x, params: Optional[CutMaxParams] = None, seed: int = 0, nuc
                            params or CutMaxParams(), 0)
 
 
+# ---- analysis (csrc/analysis_kernel.cuh) ---------------------------------
+def convergence_trace_batch_device(x, params: Optional[CutMaxParams] = None, stream=None):
+    """convergenceTrace for CUDA rows: returns (out [B, T, 4] = {mu, s2, U,
+    fraction below mean} per iteration, status [B])."""
+    torch = _torch()
+    if x.dim() != 2 or not x.is_cuda or x.dtype != torch.float64:
+        raise InvalidParamsError("x must be a 2-D float64 CUDA tensor")
+    params = params or CutMaxParams()
+    B, n = x.shape
+    out = torch.zeros((B, params.T, 4), dtype=torch.float64, device=x.device)
+    status = torch.empty(B, dtype=torch.int32, device=x.device)
+    prm = params.lower()
+    raise_for_status(_lib.pam_convergence_trace_batch_f64(x.data_ptr(), x.stride(0), B, n, C.byref(prm),
+                                                          out.data_ptr(), status.data_ptr(), _stream_ptr(stream)),
+                     what="convergence_trace_batch_device")
+    return out, status
+
+
+def convergenceTrace(x, params: Optional[CutMaxParams] = None):
+    """convergenceTrace on the GPU: one dict per iteration with
+    mu, s2, dispersion (non-top U) and fractionBelowMean."""
+    torch = _torch()
+    xv = torch.as_tensor(np.asarray(x, dtype=np.float64), device="cuda")[None, :]
+    out, st = convergence_trace_batch_device(xv, params)
+    raise_for_status(int(st.item()))
+    o = out[0].cpu().numpy()
+    return [dict(mu=float(r[0]), s2=float(r[1]), dispersion=float(r[2]), fractionBelowMean=float(r[3])) for r in o]
+
+
+def cutmax_jvp_batch_device(x, v, params: Optional[CutMaxParams] = None, want_z: bool = False, stream=None):
+    """Forward-mode JVP of CutMax for CUDA rows x in directions v (same shape):
+    returns (z or None, dz, status)."""
+    torch = _torch()
+    if x.shape != v.shape or x.dim() != 2 or not (x.is_cuda and v.is_cuda) or x.dtype != torch.float64 \
+            or v.dtype != torch.float64:
+        raise InvalidParamsError("x, v must be 2-D float64 CUDA tensors of one shape")
+    x = x.contiguous()
+    v = v.contiguous()
+    params = params or CutMaxParams()
+    B, n = x.shape
+    dz = torch.empty_like(x)
+    z = torch.empty_like(x) if want_z else None
+    status = torch.empty(B, dtype=torch.int32, device=x.device)
+    prm = params.lower()
+    raise_for_status(_lib.pam_cutmax_jvp_batch_f64(x.data_ptr(), v.data_ptr(), n, B, n, C.byref(prm),
+                                                   z.data_ptr() if z is not None else None, dz.data_ptr(), n,
+                                                   status.data_ptr(), _stream_ptr(stream)),
+                     what="cutmax_jvp_batch_device")
+    return z, dz, status
+
+
+def _check_rows(status):
+    st = status.cpu().numpy()
+    bad = np.nonzero(st)[0]
+    if bad.size:
+        raise_for_status(int(st[bad[0]]), row=int(bad[0]))
+
+
+def cutmaxJvp(x, v, params: Optional[CutMaxParams] = None) -> np.ndarray:
+    """cutmaxJvp: d cutmax(x)/dx . v on the GPU (forward mode)."""
+    torch = _torch()
+    xv = torch.as_tensor(np.asarray(x, dtype=np.float64), device="cuda")[None, :]
+    vv = torch.as_tensor(np.asarray(v, dtype=np.float64), device="cuda")[None, :]
+    _, dz, st = cutmax_jvp_batch_device(xv, vv, params)
+    _check_rows(st)
+    return dz[0].cpu().numpy()
+
+
+def cutmaxJacobian(x, params: Optional[CutMaxParams] = None) -> np.ndarray:
+    """cutmaxJacobian: J[i, j] = dZ_i/dx_j from n JVPs with the
+    basis directions, one batched launch."""
+    torch = _torch()
+    xh = np.asarray(x, dtype=np.float64)
+    n = xh.shape[0]
+    X = torch.as_tensor(xh, device="cuda")[None, :].repeat(n, 1)
+    V = torch.eye(n, dtype=torch.float64, device="cuda")
+    _, dz, st = cutmax_jvp_batch_device(X, V, params)
+    _check_rows(st)
+    return dz.cpu().numpy().T.copy()
+
+
 # ---- logit files (SPEC.md:530-551; csrc/ingest.cpp) --------------------------------
 def _read_file(path: str, pinned: bool):
     info = _abi.pam_ingest_info()

@@ -393,3 +393,73 @@ def test_violation_experiment_gpu(cuda, pam, orc):
         assert abs((1.0 - ins_g.mean()) - out["gumbelPerPrompt"][i]) < 1e-12
     with pytest.raises(pam.InvalidParamsError):
         pam.violationExperiment(prompts[:1], cfg, draws=0)
+
+
+# ---------------------------------------------------------------- §8f ---------
+def test_convergence_trace_gpu(cuda, pam, orc):
+    """convergenceTrace on the GPU vs the oracle: mu, s2,
+    non-top dispersion U and the fraction below the mean per iteration; the
+    SPEC examples (two-level input -> U = 0; random normal n=1024 -> fraction
+    > 0.5 at iteration 1; U non-increasing when c > sqrt(n-1))."""
+    torch = cuda
+    rng = np.random.default_rng(30)
+    prm = pam.CutMaxParams(T=4)
+    for n in (2, 7, 1024, 9000, 32768, 151936):
+        X = rng.normal(0, 3, (3, n))
+        out, st = pam.convergence_trace_batch_device(torch.as_tensor(X, device="cuda"), prm)
+        out = out.cpu().numpy()
+        assert np.all(st.cpu().numpy() == 0)
+        for r in range(3):
+            s, ref = orc.convergence_trace(X[r], prm.lower())
+            assert s == 0
+            np.testing.assert_allclose(out[r, :, 0], ref[:, 0], rtol=1e-12, atol=1e-13)
+            np.testing.assert_allclose(out[r, :, 1], ref[:, 1], rtol=1e-11)
+            np.testing.assert_allclose(out[r, :, 2], ref[:, 2], rtol=1e-9, atol=1e-9)
+            assert np.all(np.abs(out[r, :, 3] - ref[:, 3]) <= 1.0 / n + 1e-15)  # +-1 element at y == mu
+    tr = pam.convergenceTrace([0.9, 0.05, 0.05, 0.05], pam.CutMaxParams(T=3))
+    assert all(abs(s["dispersion"]) < 1e-12 for s in tr)  # two-level input
+    tr = pam.convergenceTrace(rng.normal(size=1024), pam.CutMaxParams(T=2))
+    assert tr[0]["fractionBelowMean"] > 0.5 or tr[1]["fractionBelowMean"] > 0.5
+    x = rng.normal(size=64)
+    tr = pam.convergenceTrace(x, pam.CutMaxParams(c=9.0, T=5, guarantee=True))
+    U = [s["dispersion"] for s in tr]
+    assert all(U[i + 1] <= U[i] + 1e-12 for i in range(len(U) - 1))
+    with pytest.raises(pam.DegenerateInputError):
+        pam.convergenceTrace(np.full(16, 2.0), prm)
+
+
+def test_cutmax_jvp_gpu(cuda, pam, orc):
+    """cutmaxJvp on the GPU vs the oracle's forward mode, v = 0 /
+    all-ones, linearity, finite differences, the Jacobian's row-sum-zero (in v =
+    ones) and SingularityError."""
+    torch = cuda
+    rng = np.random.default_rng(31)
+    prm = pam.CutMaxParams(T=4)
+    for n in (2, 33, 1000, 8192, 151936):
+        X = rng.normal(0, 2, (4, n))
+        Vd = rng.normal(size=(4, n))
+        z, dz, st = pam.cutmax_jvp_batch_device(torch.as_tensor(X, device="cuda"),
+                                                torch.as_tensor(Vd, device="cuda"), prm, want_z=True)
+        z, dz = z.cpu().numpy(), dz.cpu().numpy()
+        assert np.all(st.cpu().numpy() == 0)
+        for r in range(4):
+            s, zr, dzr = orc.cutmax_jvp(X[r], Vd[r], prm.lower())
+            assert s == 0
+            assert normwise(z[r], zr) <= 1e-12
+            assert np.max(np.abs(dz[r] - dzr)) <= 1e-9 * max(np.max(np.abs(dzr)), 1e-300) + 1e-14
+    x = rng.normal(size=48)
+    assert np.all(pam.cutmaxJvp(x, np.zeros(48), prm) == 0.0)
+    assert np.max(np.abs(pam.cutmaxJvp(x, np.ones(48), prm))) < 1e-11
+    v1, v2 = rng.normal(size=48), rng.normal(size=48)
+    a, b = pam.cutmaxJvp(x, v1, prm), pam.cutmaxJvp(x, v2, prm)
+    np.testing.assert_allclose(pam.cutmaxJvp(x, 2 * v1 - 3 * v2, prm), 2 * a - 3 * b, atol=1e-10)
+    h = 1e-5
+    zp, _, _ = orc.cutmax_batch((x + h * v1)[None, :], prm.lower())
+    zm, _, _ = orc.cutmax_batch((x - h * v1)[None, :], prm.lower())
+    assert np.max(np.abs((zp[0] - zm[0]) / (2 * h) - a)) <= 1e-4 * np.max(np.abs(a)) + 1e-9
+    J = pam.cutmaxJacobian(x, prm)
+    assert J.shape == (48, 48)
+    np.testing.assert_allclose(J @ v1, a, atol=1e-10)
+    assert np.max(np.abs(J.sum(axis=1))) < 1e-10  # shift invariance: J . ones = 0
+    with pytest.raises(pam.SingularityError):
+        pam.cutmaxJvp(np.full(16, 1.0), np.ones(16), prm)

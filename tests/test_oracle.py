@@ -324,3 +324,31 @@ def test_beta_cut_zero_violations_peaked(orc, pam):
         _, ins_g, _ = orc.sample_batch(X, cfg, prm, gumbel=True)
         gum_v += int((ins_g == 0).sum())
     assert beta_v == 0 and gum_v > 0
+
+
+def test_cutmax_jvp_oracle(orc, pam):
+    """cutmaxJvp (§8f rank 4): v = 0 -> 0, v = 1 -> 0 (shift
+    invariance), linear in v, and central finite differences (h = 1e-5) within
+    1e-4 relative on random (x, v), n <= 64."""
+    rng = np.random.default_rng(21)
+    prm = params(pam, p=3, c=5.0, T=4)
+    for trial in range(40):
+        n = int(rng.integers(2, 65))
+        x = rng.normal(0, 2, n)
+        st, z, dz = orc.cutmax_jvp(x, np.zeros(n), prm)
+        assert st == 0 and np.all(dz == 0.0)
+        st, _, dz1 = orc.cutmax_jvp(x, np.ones(n), prm)
+        assert st == 0 and np.max(np.abs(dz1)) < 1e-11
+        v1, v2 = rng.normal(size=n), rng.normal(size=n)
+        _, _, a = orc.cutmax_jvp(x, v1, prm)
+        _, _, b = orc.cutmax_jvp(x, v2, prm)
+        _, _, ab = orc.cutmax_jvp(x, 2.0 * v1 - 3.0 * v2, prm)
+        assert np.max(np.abs(ab - (2.0 * a - 3.0 * b))) <= 1e-10 * max(1.0, np.max(np.abs(ab)))
+        h = 1e-5
+        zp, _, _ = orc.cutmax_batch((x + h * v1)[None, :], prm)
+        zm, _, _ = orc.cutmax_batch((x - h * v1)[None, :], prm)
+        fd = (zp[0] - zm[0]) / (2 * h)
+        # relative 1e-4 (SPEC.md:507) above the finite-difference noise floor ~eps/h
+        assert np.max(np.abs(fd - a)) <= 1e-4 * np.max(np.abs(a)) + 1e-9
+    st, _, _ = orc.cutmax_jvp(np.full(8, 2.5), np.ones(8), prm)
+    assert st == pam._abi.PAM_ERR_SINGULAR
