@@ -102,7 +102,8 @@ struct __align__(16) XchChannel {
 struct __align__(16) Bcast {
   double ke, be, dm, re;
   int flag;  // 1: the exact second pass about dm is needed first
-  int pad[3];
+  int st;    // row status so far (generic flow)
+  int pad[2];
 };
 
 struct __align__(16) ControlBlock {
@@ -545,9 +546,8 @@ __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, c
     if (FIRST) ptx::fence_proxy_async_smem();  // side writes -> visible to the TMA engine after the barrier
   };
 
-  // ---- T iterations; the last one (no variance; argmax) is peeled -----------
-  double total = 0.0;
-  for (int t = 0; t < T; ++t) {
+  // scalar chain of iteration t from (kcur, dm, s2): status, 1/sigma, k, b
+  auto chain = [&](int t, double& kd, double& bd) {
     const double mu = kcur + dm;
     // status: first failure wins (branch-free on the common path)
     const bool bad_range = !isfinite(mu) || !isfinite(s2);
@@ -567,8 +567,29 @@ __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, c
         if (rs) st = rs;
       }
     }
-    const double kd = (st == PAM_OK) ? inv_sigma * c_inv : 0.0;
-    const double bd = fma(-dm, kd, 1.0);
+    kd = (st == PAM_OK) ? inv_sigma * c_inv : 0.0;
+    bd = fma(-dm, kd, 1.0);
+  };
+  // control warp: warp 0 alone waits for each exchange, runs the moments, the
+  // guard decision and the chain, and broadcasts (k, b, dm, status) through
+  // shared memory (named barrier 1); see the p = 3 flow of cutmax_rows_kernel
+  const int warp = gtid >> 5;
+  auto bar1 = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(NTG) : "memory"); };
+  auto publish = [&](double kd, double bd, int flag) {
+    if ((gtid & 31) == 0) {
+      cb->bc.ke = kd;
+      cb->bc.be = bd;
+      cb->bc.dm = dm;
+      cb->bc.flag = flag;
+      cb->bc.st = st;
+    }
+  };
+
+  // ---- T iterations; the last one (no variance; argmax) is peeled -----------
+  double total = 0.0;
+  double kd, bd;
+  chain(0, kd, bd);  // every warp: identical inputs
+  for (int t = 0; t < T; ++t) {
     const Elem ke = (Elem)kd, be = affine_coef<Elem>(bd, dm), kn = (Elem)(-knext);
     const int p = pcur;
     w = cutmax_update<Elem, P>(w, ke, be, kn, p);
@@ -587,13 +608,50 @@ __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, c
       PAM_TRACE(tr, 5 + 2 * t);
       xch_push<NTG, kSum2>((double)sa + (double)sb, (double)qa + (double)qb, 0.0, 0LL, cb, xround, rank, C, gtid,
                            [&]() { h.side(t); });
-      double bv = 0.0;
-      long long bi = 0;
-      const double2 r = xch_wait<kSum2>(bv, bi, cb, xround, C, gtid);
-      PAM_TRACE(tr, 6 + 2 * t);
-      const double wd = (double)w;
-      guard(r.x - mph * wd, r.y - mph * wd * wd, wd, dm, s2);
       kcur = kthis;
+      const double wd = (double)w;
+      if (warp == 0) {
+        double bv = 0.0;
+        long long bi = 0;
+        const double2 r = xch_wait<kSum2>(bv, bi, cb, xround, C, gtid);
+        const double Q = r.y - mph * wd * wd;
+        moments_from_sums(r.x - mph * wd, Q, inv_n, dm, s2);
+        if (st == PAM_OK && isfinite(Q) && Q * inv_n > kGuard * s2) {
+          publish(0.0, 0.0, 1);  // exact second pass first
+        } else {
+          chain(t + 1, kd, bd);
+          publish(kd, bd, 0);
+        }
+      } else {
+        ++xround;  // keep the round counter in step with warp 0
+      }
+      bar1();
+      Bcast b = cb->bc;
+      if (b.flag) {  // exact second pass about dm (cluster-uniform, rare)
+        dm = b.dm;
+        const Elem dme = (Elem)dm;
+        Elem q2a = 0, q2b = 0;
+#pragma unroll
+        for (int i = 0; i < E; i += 2) {
+          const Elem d0 = v[i] - dme, d1 = v[i + 1] - dme;
+          if (real(i)) q2a = fma_e(d0, d0, q2a);
+          if (real(i + 1)) q2b = fma_e(d1, d1, q2b);
+        }
+        const double2 r2 = cluster_sum2<NTG>((double)q2a + (double)q2b, 0.0, cb, xround, rank, C, gtid);
+        if (warp == 0) {
+          const Elem dw = (Elem)w - dme;
+          s2 = (r2.x - mph * (double)dw * (double)dw) * inv_n;
+          chain(t + 1, kd, bd);
+          publish(kd, bd, 0);
+        }
+        bar1();
+        b = cb->bc;
+      }
+      kd = b.ke;
+      bd = b.be;
+      dm = b.dm;
+      st = b.st;
+      PAM_TRACE(tr, 6 + 2 * t);
     } else {
       if (first)
         pass(BoolC<true>(), BoolC<true>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);

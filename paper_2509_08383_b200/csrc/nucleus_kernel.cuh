@@ -34,6 +34,7 @@ struct SamplerArgs {
   uint64_t seed, draw;
   int32_t tma;  // 1: TMA bulk load (16-byte aligned rows), 0: thread copy
   double inv_n;
+  long long* trace;  // debug phase stamps (trace builds)
   RowParams rp;
 };
 
@@ -80,7 +81,16 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
   uint32_t xround = 0, load_par = 0, g_par = 0;
   double v[E];
 
-  for (int64_t row = cid; row < a.B; row += ncl) {
+  int64_t lrow = 0;
+  for (int64_t row = cid; row < a.B; row += ncl, ++lrow) {
+#ifdef PAM_TRACE_BUILD
+    long long* tr =
+        (a.trace && lrow < kTraceRows) ? a.trace + ((int64_t)blockIdx.x * kTraceRows + lrow) * kTraceEvents : nullptr;
+#else
+    long long* tr = nullptr;
+#endif
+    const int gtid = tid;
+    PAM_TRACE(tr, 0);
     const double* xrow = a.x + row * a.ldx;
     const double K0 = __ldg(xrow);
     __syncthreads();  // landing buffer and wred of the previous row retired
@@ -102,6 +112,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
       v[k * VEC + 0] = GUMBEL ? gumbel_from_u(u0) : beta_icdf(u0, a.inv_alpha);
       v[k * VEC + 1] = GUMBEL ? gumbel_from_u(u1) : beta_icdf(u1, a.inv_alpha);
     }
+    PAM_TRACE(tr, 1);
     if (a.tma) {
       ptx::mbar_wait_cta(bar_load, load_par);
       load_par ^= 1u;
@@ -132,6 +143,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
       }
     }
 
+    PAM_TRACE(tr, 2);
     double rnorm = 1.0;
     long long unused_argmax;
     const double2 part = input_pass<double, E>(v, K0);
@@ -143,6 +155,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     int st = cutmax_iterate<double, NT, E, P, false>(v, rin.x, rin.y, K0, len, (double)((int64_t)C * NT * E - n), a.rp, a.inv_n, cb, xround, rank, C,
                                                      tid, base, nullptr, rnorm, unused_argmax, hooks, nullptr);
 
+    PAM_TRACE(tr, 3);
     // token candidate over Z = Y * rnorm (and optional one-hot store)
     double best = -HUGE_VAL, bestx = 0.0;
     long long besti = 0x7fffffffffffffffLL;
@@ -224,6 +237,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
       xmax = __shfl_sync(0xffffffffu, xmax, 0);
     }
 
+    PAM_TRACE(tr, 4);
     // nucleus membership: sum over x_k > x_tok of exp(x_k - max) vs p * total
     double tot = 0.0, above = 0.0;
 #pragma unroll
@@ -240,6 +254,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
       }
     }
     const double2 ta = cluster_sum2<NT>(tot, above, cb, xround, rank, C, tid);
+    PAM_TRACE(tr, 5);
     if (rank == 0 && tid == 0) {
       if (a.token) a.token[row] = (st == PAM_OK) ? (int32_t)besti : -1;
       if (a.inside) a.inside[row] = (st == PAM_OK && ta.y < a.p_nucleus * ta.x) ? 1 : 0;

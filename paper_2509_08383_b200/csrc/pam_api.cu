@@ -307,6 +307,7 @@ int sampler_batch_impl(const double* d_x, int64_t ld_x, int64_t B, int64_t n, co
   sa.inv_n = 1.0 / (double)n;
   sa.tma = ((uintptr_t)d_x % 16 == 0) && (ld_x % 2 == 0) && (n % 2 == 0) && getenv("PAM_DISABLE_TMA") == nullptr;
   fill_row_params(prm, &sa.rp);
+  if (g_trace && (int64_t)clusters * C * kTraceRows * kTraceEvents <= g_trace_entries) sa.trace = g_trace;
   return launch_cluster_kernel(fn, var->nt, C, clusters, smem, stream, &sa);
 }
 
