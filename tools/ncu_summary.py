@@ -22,6 +22,8 @@ KEYS = [
     "launch__block_size", "launch__cluster_dim_x", "launch__shared_mem_per_block_dynamic",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum", "sm__cycles_elapsed.avg",
     "lts__t_bytes.sum", "smsp__average_warp_latency_issue_stalled_barrier", "sm__ctas_launched.sum",
+    "l1tex__m_l1tex2xbar_write_bytes_mem_dshared.sum", "l1tex__m_l1tex2xbar_req_cycles_active_mem_dshared.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
 ]
 
 
