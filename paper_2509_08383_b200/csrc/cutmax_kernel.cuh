@@ -1082,6 +1082,13 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         else
           pass(BoolC<false>(), ke, be, kn, part);
         PAM_TRACE(tr, 5 + 2 * t);
+#ifdef PAM_TRACE_BUILD
+        if (tr != nullptr && t == 1) {  // pass-end stamps of warps 0, 5, 10, 15 (intra-CTA skew)
+          if (gtid == 5 * 32) tr[30] = clock64();
+          if (gtid == 10 * 32) tr[31] = clock64();
+          if (gtid == NTG - 32) tr[19] = clock64();
+        }
+#endif
         if (need3)
           xch_push<NTG, kSum3>(part.x, part.y, part.z, 0LL, cb, xround, rank, C, gtid, [&]() { side(t); });
         else

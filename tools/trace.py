@@ -65,6 +65,10 @@ def run(B, n, dtype, cfg=None, T=4):
         d = (rows[:, :, b_] - rows[:, :, a_]).ravel()
         print(f"   xchg {t} wait spread: min {np.min(d):6.0f} p10 {np.percentile(d, 10):6.0f} med {np.median(d):6.0f} "
               f"p90 {np.percentile(d, 90):6.0f} max {np.max(d):6.0f}")
+    for k, nm in ((30, "warp 5"), (31, "warp 10"), (19, "warp 15")):
+        d = (rows[:, :, k] - rows[:, :, 7]).ravel()  # vs warp 0's pass-1 end (event 7)
+        print(f"   pass-1 end, {nm} - warp 0: med {np.median(d):6.0f} p10 {np.percentile(d, 10):6.0f} "
+              f"p90 {np.percentile(d, 90):6.0f}")
     print(f"   {'-> next row start':28s} {np.median(tr[:, 2:8, 0] - tr[:, 1:7, 21]):8.0f} cyc")
     print(f"   {'row period':28s} {period:8.0f} cyc  {period / CLK:6.2f} us")
     os.environ.pop(key, None)
