@@ -14,6 +14,7 @@
 
 #include "../../include/pam_c_api.h"
 #include "analysis_kernel.cuh"
+#include "cutmax_ahead_kernel.cuh"
 #include "cutmax_kernel.cuh"
 #include "nucleus_kernel.cuh"
 #include "pam_variants.h"
@@ -202,6 +203,82 @@ int fill_row_params(const pam_cutmax_params* prm, RowParams* rp) {
   return PAM_OK;
 }
 
+// Geometry of the two-iterations-per-exchange kernel (cutmax_ahead_kernel.cuh).
+// Same scoring as choose_geometry: rows per microsecond = clusters / t_row with
+// t_row ~= a + b * cap * k; a (two exchanges + chains per row) = 2.6 us,
+// b ~= 36 fp64 instructions per element slot at 64/clk/SM = 0.33 ns.
+// Dev override: PAM_FORCE_AHEAD = "NTG,E,C".
+struct AheadGeometry {
+  const AheadVariant* var = nullptr;
+  int C = 0, L = 0;
+};
+int ahead_smem_bytes(const AheadVariant& v) { return ((v.ntg * v.e * 8 + 127) / 128) * 128 + v.ctl_bytes; }
+
+AheadGeometry choose_ahead_geometry(int64_t B, int64_t n) {
+  AheadGeometry g;
+  if (const char* fs = getenv("PAM_FORCE_AHEAD")) {
+    int ntg = 0, e = 0, c = 0;
+    if (sscanf(fs, "%d,%d,%d", &ntg, &e, &c) == 3) {
+      for (int i = 0; i < kNumAheadVariants; ++i) {
+        const AheadVariant& v = kAheadVariants[i];
+        const int64_t L = slice_len(n, c, 2);
+        if (v.ntg == ntg && v.e == e && (int64_t)v.ntg * v.e >= L) {
+          g.var = &v;
+          g.C = c;
+          g.L = (int)L;
+          return g;
+        }
+      }
+    }
+  }
+  int dev = 0;
+  const bool have_gpu = cudaGetDevice(&dev) == cudaSuccess;
+  int nsm = 148;
+  if (have_gpu && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
+  const double a_us = 2.6, b_ns = 0.33;
+  double best_score = -1.0;
+  for (int C = 1; C <= 16; ++C) {
+    const int64_t L = slice_len(n, C, 2);
+    for (int i = 0; i < kNumAheadVariants; ++i) {
+      const AheadVariant& v = kAheadVariants[i];
+      const int64_t cap = (int64_t)v.ntg * v.e;
+      if (cap < L || (C > 1 && cap > L + L * 3 / 10)) continue;
+      if (C > 1 && L < 2048) continue;
+      const int smem = ahead_smem_bytes(v);
+      if (smem > 227 * 1024) continue;
+      const int active = have_gpu ? max_active_clusters(v.fn, v.ntg, C, smem) : nsm / C;
+      if (active <= 0) continue;
+      const int64_t clusters = (B < active) ? B : active;
+      const int64_t k = (clusters * C + nsm - 1) / nsm;
+      const double t_us = a_us + 1e-3 * b_ns * (double)cap * (double)(k < 1 ? 1 : k);
+      const double score = (double)clusters / t_us - 1e-9 * (double)C;
+      if (score > best_score) {
+        best_score = score;
+        g.var = &v;
+        g.C = C;
+        g.L = (int)L;
+      }
+    }
+  }
+  cudaGetLastError();
+  return g;
+}
+
+// The ahead kernel serves fp64, p = 3 everywhere, exact scalars, normalised
+// output without the stats side output, on TMA-aligned rows.
+bool ahead_eligible(const pam_cutmax_params* prm, bool tma, const double* d_stats) {
+  // Opt-in until it beats cutmax_rows_kernel on the headline shape:
+  // PAM_ENABLE_AHEAD=1 (or PAM_FORCE_AHEAD=NTG,E,C) selects it.
+  if (!getenv("PAM_ENABLE_AHEAD") && !getenv("PAM_FORCE_AHEAD")) return false;
+  if (!tma || d_stats || getenv("PAM_DISABLE_AHEAD") || getenv("PAM_FORCE_CFG_F64") || getenv("PAM_FORCE_GENERIC_P"))
+    return false;
+  if (prm->flags & PAM_F_NO_NORMALIZE) return false;
+  if (prm->invsqrt_mode != PAM_MODE_EXACT || prm->inv_mode != PAM_MODE_EXACT) return false;
+  for (int t = 0; t < prm->T; ++t)
+    if (prm->p[t] != 3) return false;
+  return true;
+}
+
 template <typename Elem>
 int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const pam_cutmax_params* prm, Elem* d_z,
                       int64_t ld_z, int32_t* d_argmax, int32_t* d_status, double* d_stats, cudaStream_t stream) {
@@ -212,11 +289,39 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   if (prm->eps_stop > 0.0) return PAM_ERR_UNSUPPORTED;
   if (B == 0) return PAM_OK;
   if (n > (int64_t)1 << 30) return PAM_ERR_UNSUPPORTED;
-  const Geometry g = choose_geometry((int)sizeof(Elem), B, n);
-  if (!g.var) return PAM_ERR_UNSUPPORTED;
   const int vec = 16 / (int)sizeof(Elem);
   const bool tma = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_z % 16 == 0) && (ld_x % vec == 0) &&
                    (ld_z % vec == 0) && (n % vec == 0) && getenv("PAM_DISABLE_TMA") == nullptr;
+  if (sizeof(Elem) == 8 && ahead_eligible(prm, tma, d_stats)) {
+    const AheadGeometry ag = choose_ahead_geometry(B, n);
+    if (ag.var) {
+      const int smem = ahead_smem_bytes(*ag.var);
+      const int maxcl = max_active_clusters(ag.var->fn, ag.var->ntg, ag.C, smem);
+      if (maxcl <= 0) return cuda_fail(cudaErrorInvalidConfiguration, "no cluster fits (occupancy 0)");
+      const int clusters = (int)(B < maxcl ? B : maxcl);
+      CutmaxArgs ka;
+      memset(&ka, 0, sizeof ka);
+      ka.x = d_x;
+      ka.z = d_z;
+      ka.argmax = d_argmax;
+      ka.status = d_status;
+      ka.ldx = ld_x;
+      ka.ldz = ld_z;
+      ka.B = B;
+      ka.n = n;
+      ka.L = ag.L;
+      ka.ctrl_offset = ((ag.var->ntg * ag.var->e * 8 + 127) / 128) * 128;
+      ka.tma = 1;
+      ka.inv_n = 1.0 / (double)n;
+      const char* df = getenv("PAM_DEBUG_FLAGS");
+      ka.debug_flags = df ? atoi(df) : 0;
+      fill_row_params(prm, &ka.rp);
+      if (g_trace && (int64_t)clusters * ag.C * kTraceRows * kTraceEvents <= g_trace_entries) ka.trace = g_trace;
+      return launch_cluster_kernel(ag.var->fn, ag.var->ntg, ag.C, clusters, smem, stream, &ka);
+    }
+  }
+  const Geometry g = choose_geometry((int)sizeof(Elem), B, n);
+  if (!g.var) return PAM_ERR_UNSUPPORTED;
   bool p3 = getenv("PAM_FORCE_GENERIC_P") == nullptr;  // dev knob: A/B the generic-p kernel
   for (int t = 0; t < prm->T; ++t) p3 = p3 && (prm->p[t] == 3);
   const void* fn = g.var->fn[p3 ? 1 : 0];
@@ -595,6 +700,23 @@ int pam_cutmax_jvp_batch_f64(const double* d_x, const double* d_v, int64_t ld_x,
 int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_params* prm, pam_launch_info* info) {
   if (!info || (dtype_bytes != 4 && dtype_bytes != 8)) return PAM_ERR_BAD_ARGUMENT;
   memset(info, 0, sizeof *info);
+  if (dtype_bytes == 8 && prm && n % 2 == 0 && ahead_eligible(prm, true, nullptr)) {
+    const AheadGeometry ag = choose_ahead_geometry(B, n);
+    if (ag.var) {
+      const int smem = ahead_smem_bytes(*ag.var);
+      info->threads = ag.var->ntg;
+      info->elems_per_thread = ag.var->e;
+      info->cluster = ag.C;
+      info->smem_bytes = smem;
+      info->tma = 1;
+      const int maxcl = max_active_clusters(ag.var->fn, ag.var->ntg, ag.C, smem);
+      info->clusters = (int)(B < maxcl ? B : maxcl);
+      info->ctas = info->clusters * ag.C;
+      info->groups = 1;
+      info->kernel_id = 1000 + (int)(ag.var - kAheadVariants);  // 1000+: the two-iterations-per-exchange kernel
+      return PAM_OK;
+    }
+  }
   const Geometry g = choose_geometry(dtype_bytes, B, n);
   if (!g.var) return PAM_ERR_UNSUPPORTED;
   bool p3 = true;

@@ -98,6 +98,13 @@ __device__ __forceinline__ void st_async_f64x2(uint32_t remote_addr, double a, d
       : "memory");
 }
 
+// 8-byte DSMEM push (one exchange sum) completing 8 tx-bytes on the destination's mbarrier.
+__device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double a, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(remote_addr),
+               "l"(__double_as_longlong(a)), "r"(remote_bar)
+               : "memory");
+}
+
 __device__ __forceinline__ void st_async_b64x2(uint32_t remote_addr, uint64_t a, uint64_t b, uint32_t remote_bar) {
   asm volatile(
       "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(remote_addr),

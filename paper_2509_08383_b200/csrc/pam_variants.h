@@ -22,7 +22,16 @@ struct SamplerVariant {
   const void* fn[2][2];  // [P==3][GUMBEL]
 };
 
+// Two-iterations-per-exchange fp64 p = 3 kernel (cutmax_ahead_kernel.cuh).
+struct AheadVariant {
+  int ntg, e;
+  int ctl_bytes;  // sizeof(AhCtl<ntg>)
+  const void* fn;
+};
+
 extern const Variant kCutmaxVariants[];
+extern const AheadVariant kAheadVariants[];
+extern const int kNumAheadVariants;
 extern const int kNumCutmaxVariants;
 extern const AnalysisVariant kAnalysisVariants[];
 extern const int kNumAnalysisVariants;

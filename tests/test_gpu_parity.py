@@ -463,3 +463,60 @@ def test_cutmax_jvp_gpu(cuda, pam, orc):
     assert np.max(np.abs(J.sum(axis=1))) < 1e-10  # shift invariance: J . ones = 0
     with pytest.raises(pam.SingularityError):
         pam.cutmaxJvp(np.full(16, 1.0), np.ones(16), prm)
+
+
+# ------------------------------------------- two-iterations-per-exchange ---
+@pytest.fixture
+def ahead_on():
+    """Select cutmax_ahead_kernel (fp64, p = 3, exact scalars; opt-in)."""
+    os.environ["PAM_ENABLE_AHEAD"] = "1"
+    yield
+    del os.environ["PAM_ENABLE_AHEAD"]
+
+
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 6])
+def test_ahead_kernel_T_sweep(cuda, pam, orc, ahead_on, T):
+    """Every stage shape: T=1 (one-iteration last stage), T=2 (one exchange
+    per row, S_1..S_9 of the input), T=3/5 (mid + one-iteration last), T=4/6."""
+    x = W.gaussian(12, 32768, seed=60 + T)
+    prm = pam.CutMaxParams(T=T)
+    z, am, st = gpu_cutmax(cuda, pam, x, prm)
+    zr, amr, str_ = orc.cutmax_batch(x, prm.lower())
+    check_rows(z, am, st, zr, amr, str_, tol64_for([3] * T))
+
+
+@pytest.mark.parametrize("case", ["zipf151936", "planted", "pipeline", "cauchy", "small_c", "tiny"])
+def test_ahead_kernel_parity(cuda, pam, orc, ahead_on, case):
+    """BASELINE shapes, near-ties, the row pipeline with degenerate / non-finite /
+    offset rows, heavy tails (exercises the exact fallback) and small c."""
+    T, c = 4, 5.0
+    if case == "zipf151936":
+        x = W.zipf_logits(8, 151936, seed=70)
+    elif case == "planted":
+        x, istar, _ = W.planted(64, 32768, seed=71)
+        T = 3
+    elif case == "pipeline":
+        x = W.gaussian(700, 6000, seed=72)
+        x[5] += 300.0
+        x[6, :] = 2.5
+        x[9, 3] = np.nan
+        x[11, 0] = 40.0  # poor input shift sample
+    elif case == "cauchy":
+        x = np.random.default_rng(73).standard_cauchy((16, 32768))
+    elif case == "small_c":
+        x = W.gaussian(16, 4096, seed=74)
+        c = 1.5
+    else:
+        x = W.gaussian(5, 2, seed=75)
+    prm = pam.CutMaxParams(T=T, c=c)
+    z, am, st = gpu_cutmax(cuda, pam, x, prm)
+    zr, amr, str_ = orc.cutmax_batch(x, prm.lower())
+    check_rows(z, am, st, zr, amr, str_, TOL64)
+    if case == "planted":
+        assert np.array_equal(am, istar)
+
+
+def test_ahead_kernel_selected(cuda, pam, ahead_on):
+    """The opt-in really launches the ahead kernel (kernel ids >= 1000)."""
+    info = pam.launch_info(8, 4096, 151936, pam.CutMaxParams())
+    assert info["kernel_id"] >= 1000 and info["cluster"] >= 2
