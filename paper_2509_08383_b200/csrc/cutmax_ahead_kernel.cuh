@@ -155,26 +155,6 @@ __device__ __forceinline__ double ah_rcp(double x) {
   return r;
 }
 
-// Warp argmax in the (value desc, index asc) order with three REDUX steps on a
-// monotone 64-bit key of the value (+0.0 and -0.0 compare equal, as in
-// cand_better).  Every lane returns the winner; NaN candidates never occur
-// (the passes only admit y > best).
-__device__ __forceinline__ void ah_warp_argmax(double& v, long long& ix) {
-  constexpr unsigned FULL = 0xffffffffu;
-  unsigned long long b = (unsigned long long)__double_as_longlong(v + 0.0);
-  b = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
-  const unsigned mhi = __reduce_max_sync(FULL, hi);
-  const unsigned mlo = __reduce_max_sync(FULL, hi == mhi ? lo : 0u);
-  const bool win = hi == mhi && lo == mlo;
-  const unsigned i32 = (win && ix >= 0 && ix < 0xffffffffLL) ? (unsigned)ix : 0xffffffffu;
-  const unsigned mi = __reduce_min_sync(FULL, i32);
-  unsigned long long k = ((unsigned long long)mhi << 32) | mlo;
-  k = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-  v = __longlong_as_double((long long)k);
-  ix = mi == 0xffffffffu ? 0x7fffffffffffffffLL : (long long)mi;
-}
-
 // Accumulate the power sums S_1..S_M of w (s[j] holds S_{j+1}).
 template <int M>
 __device__ __forceinline__ void ah_acc(double (&s)[kAhMaxM], const double w) {
@@ -231,7 +211,7 @@ __device__ __forceinline__ void ah_push(const double (&s)[kAhMaxM], const double
   if (ARG) {  // each warp reduces its candidates first (REDUX), lane 0 posts the warp's
     double wv = bv;
     long long wi = bi;
-    ah_warp_argmax(wv, wi);
+    warp_argmax(wv, wi);
     if (lane == 0) {
       cb->candv[warp] = wv;
       cb->candi[warp] = wi;
@@ -249,7 +229,7 @@ __device__ __forceinline__ void ah_push(const double (&s)[kAhMaxM], const double
     } else {
       double v = lane < NW ? cb->candv[lane] : -HUGE_VAL;
       long long ix = lane < NW ? cb->candi[lane] : 0x7fffffffffffffffLL;
-      ah_warp_argmax(v, ix);
+      warp_argmax(v, ix);
       if (lane < (int)C)
         ptx::st_async_b64x2(ptx::mapa(ptx::smem_addr(&cb->rarg[par][rank]), (uint32_t)lane),
                             (uint64_t)__double_as_longlong(v), (uint64_t)ix, ptx::mapa(bar, (uint32_t)lane));
@@ -282,7 +262,7 @@ __device__ __forceinline__ double ah_wait(AhCtl<NTG>* cb, uint32_t& round, const
     const double2 rv = cb->rarg[par][have ? lane : 0];
     bv = have ? rv.x : -HUGE_VAL;
     bi = have ? __double_as_longlong(rv.y) : 0x7fffffffffffffffLL;
-    ah_warp_argmax(bv, bi);
+    warp_argmax(bv, bi);
   }
   ++round;
   return S;

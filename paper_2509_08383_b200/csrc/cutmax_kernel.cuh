@@ -179,17 +179,33 @@ __device__ __forceinline__ void bfly_sum2(double& a, double& b) {
   }
 }
 
+// Warp argmax in the (value desc, index asc) order of cand_better with three
+// REDUX steps on a monotone 64-bit key of the value (+0.0 and -0.0 compare
+// equal; NaN candidates never occur: the passes only admit y > best).  Every
+// lane returns the winner.  Indices must be < 2^32 - 1 (n <= 2^30); the
+// sentinel index (> that) survives only when every candidate carries it.
+__device__ __forceinline__ void warp_argmax(double& v, long long& ix) {
+  constexpr unsigned FULL = 0xffffffffu;
+  unsigned long long b = (unsigned long long)__double_as_longlong(v + 0.0);
+  b = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  const unsigned mhi = __reduce_max_sync(FULL, hi);
+  const unsigned mlo = __reduce_max_sync(FULL, hi == mhi ? lo : 0u);
+  const bool win = hi == mhi && lo == mlo;
+  const unsigned i32 = (win && ix >= 0 && ix < 0xffffffffLL) ? (unsigned)ix : 0xffffffffu;
+  const unsigned mi = __reduce_min_sync(FULL, i32);
+  unsigned long long k = ((unsigned long long)mhi << 32) | mlo;
+  k = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  v = __longlong_as_double((long long)k);
+  ix = mi == 0xffffffffu ? 0x7fffffffffffffffLL : (long long)mi;
+}
+
+// Argmax over aligned WIDTH-lane groups.  Every caller fills the lanes outside
+// a group with copies of the group or neutral candidates, so the whole-warp
+// REDUX form (warp_argmax) gives each group's result.
 template <int WIDTH>
 __device__ __forceinline__ void bfly_argmax(double& best, long long& besti) {
-#pragma unroll
-  for (int m = WIDTH / 2; m > 0; m >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, best, m);
-    const long long oi = __shfl_xor_sync(0xffffffffu, besti, m);
-    if (cand_better(ov, oi, best, besti)) {
-      best = ov;
-      besti = oi;
-    }
-  }
+  warp_argmax(best, besti);
 }
 
 // ---------------------------------------------------------------------------
