@@ -8,7 +8,7 @@ import torch
 import paper_2509_08383_b200 as pam
 from paper_2509_08383_b200 import workloads as W
 
-PEAK = 6540.2
+PEAK = 6547.5
 
 
 def time_fn(fn, reps):
