@@ -171,6 +171,12 @@ __device__ __forceinline__ bool cand_better(double v, long long i, double bv, lo
 // and the argmax rule are commutative, all lanes of a group hold bit-identical
 // values.
 template <int WIDTH>
+__device__ __forceinline__ void bfly_sum1(double& a) {
+#pragma unroll
+  for (int m = WIDTH / 2; m > 0; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
+}
+
+template <int WIDTH>
 __device__ __forceinline__ void bfly_sum2(double& a, double& b) {
 #pragma unroll
   for (int m = WIDTH / 2; m > 0; m >>= 1) {
@@ -225,20 +231,22 @@ struct NoSide {
 // slot); or two sums plus the lexicographic (value desc, index asc) argmax.
 enum XchMode { kSum2 = 0, kSum3 = 1, kArgmax = 2 };
 
+// kSum3 with third == false behaves as kSum2 (one code copy for both in the p = 3 row loop).
 template <int NTG, int MODE, typename Ch, typename Side = NoSide>
 __device__ __forceinline__ void xch_push(double a, double b, double c, long long ci_, Ch* cb,
                                          const uint32_t round, const uint32_t rank, const uint32_t C, const int gtid,
-                                         const Side& side = Side()) {
+                                         const Side& side = Side(), const bool third = true) {
   constexpr int NW = NTG / 32;
   const int lane = gtid & 31, warp = gtid >> 5;
   double c2 = 0.0;  // unused partner of c in kSum3 (keeps the butterfly a pair)
   long long ci = ci_;
   bfly_sum2<32>(a, b);
   if (MODE == kArgmax) bfly_argmax<32>(c, ci);
-  if (MODE == kSum3) bfly_sum2<32>(c, c2);
+  if (MODE == kSum3 && third) bfly_sum1<32>(c);
+  (void)c2;
   if (lane == 0) {
     cb->wred[warp] = make_double2(a, b);
-    if (MODE != kSum2) cb->wcand[warp] = make_double2(c, __longlong_as_double(ci));
+    if (MODE == kArgmax || (MODE == kSum3 && third)) cb->wcand[warp] = make_double2(c, __longlong_as_double(ci));
   }
   __syncthreads();
   const uint32_t par = round & 1u;
@@ -248,15 +256,12 @@ __device__ __forceinline__ void xch_push(double a, double b, double c, long long
     bfly_sum2<NW>(ca, cbv);
     double cv = -HUGE_VAL;
     long long cix = 0x7fffffffffffffffLL;
-    if (MODE != kSum2) {
+    if (MODE == kArgmax || (MODE == kSum3 && third)) {
       const double2 wc = cb->wcand[lane & (NW - 1)];
       cv = wc.x;
       cix = __double_as_longlong(wc.y);
       if (MODE == kArgmax) bfly_argmax<NW>(cv, cix);
-      if (MODE == kSum3) {
-        double z = 0.0;
-        bfly_sum2<NW>(cv, z);
-      }
+      if (MODE == kSum3) bfly_sum1<NW>(cv);
     }
     if (lane < (int)C) {
       const uint32_t bar = ptx::mapa(ptx::smem_addr(&cb->mb_x[par]), (uint32_t)lane);
@@ -274,7 +279,7 @@ __device__ __forceinline__ void xch_push(double a, double b, double c, long long
 // Returns (a, b); c / ci receive the third sum or the argmax.
 template <int MODE, typename Ch>
 __device__ __forceinline__ double2 xch_wait(double& c, long long& ci, Ch* cb, uint32_t& round,
-                                            const uint32_t C, const int gtid) {
+                                            const uint32_t C, const int gtid, const bool third = true) {
   const int lane = gtid & 31;
   const uint32_t par = round & 1u, ph = (round >> 1) & 1u;
   ptx::mbar_wait_cta(ptx::smem_addr(&cb->mb_x[par]), ph);
@@ -290,10 +295,9 @@ __device__ __forceinline__ double2 xch_wait(double& c, long long& ci, Ch* cb, ui
     ci = have ? __double_as_longlong(rec.cand.y) : 0x7fffffffffffffffLL;
     bfly_argmax<16>(c, ci);
   }
-  if (MODE == kSum3) {
+  if (MODE == kSum3 && third) {
     c = have ? rec.cand.x : 0.0;
-    double z = 0.0;
-    bfly_sum2<16>(c, z);
+    bfly_sum1<16>(c);
   }
   ++round;
   return make_double2(a, b);
