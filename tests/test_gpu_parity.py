@@ -520,3 +520,35 @@ def test_ahead_kernel_selected(cuda, pam, ahead_on):
     """The opt-in really launches the ahead kernel (kernel ids >= 1000)."""
     info = pam.launch_info(8, 4096, 151936, pam.CutMaxParams())
     assert info["kernel_id"] >= 1000 and info["cluster"] >= 2
+
+
+# ------------------------------------------------------------- fuzz -------
+@pytest.mark.parametrize("kernel", ["rows", "ahead"])
+def test_random_shapes_and_params(cuda, pam, orc, kernel):
+    """Seeded random (B, n, T, c, p, ld, dtype) against the oracle: odd and even n,
+    strided rows, tiny and cluster-sized slices, p = 3 and p = 5."""
+    rng = np.random.default_rng(2509 if kernel == "rows" else 8383)
+    if kernel == "ahead":
+        os.environ["PAM_ENABLE_AHEAD"] = "1"
+    try:
+        for _ in range(24):
+            B = int(rng.integers(1, 24))
+            n = int(rng.choice([2, 3, 7, 64, 1000, 1001, 4096, 9000, 20000, 40002, 65536]))
+            T = int(rng.integers(1, 7))
+            c = float(rng.choice([1.5, 5.0, 12.0, 40.0]))
+            p = 3 if kernel == "ahead" or rng.random() < 0.7 else 5
+            f32 = kernel == "rows" and rng.random() < 0.3
+            ld = n + int(rng.choice([0, 0, 0, 1, 4]))
+            x = W.gaussian(B, n, seed=int(rng.integers(1 << 30)), sigma=float(rng.choice([0.1, 3.0, 50.0])))
+            if f32:
+                x = x.astype(np.float32)
+            prm = pam.CutMaxParams(p=p, c=c, T=T)
+            z, am, st = gpu_cutmax(cuda, pam, x, prm, ld=ld)
+            zr, amr, str_ = orc.cutmax_batch(x, prm.lower())
+            if f32:
+                tol = TOL32 * max(1.0, float(p) ** T / 81.0)
+            else:
+                tol = tol64_for([p] * T)
+            check_rows(z, am, st, zr, amr, str_, tol)
+    finally:
+        os.environ.pop("PAM_ENABLE_AHEAD", None)
