@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_ahead_kernel(const CutmaxArgs a
     const double s2 = xs1(p) * inv_n;
     if (st == PAM_OK) st = status_of(kc + dm, s2);
     ca.ka = (st == PAM_OK) ? rsqrt(s2) * rp.inv_c[2 * i] : 0.0;
-    ca.aa = fma(-dm, ca.ka, 1.0);
+    ca.aa = fma(-((kc + dm) - kc), ca.ka, 1.0);  // centered on the fp64-rounded mean (see phase A)
     ca.st = st;
   };
   // exact iteration s+1 (two) from registers v = y_{s+1}, and/or the explicit
@@ -576,7 +576,10 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_ahead_kernel(const CutmaxArgs a
     const bool slow = st == PAM_OK && !(q <= kAhCondMax * s2);  // poor shift / s2 <= 0: exact statistics
     if (st == PAM_OK && !slow) st = status_of(Kc + dm, s2);
     const double ka = (st == PAM_OK && !slow) ? rsqrt(s2) * rp.inv_c[it] : 0.0;
-    const double aa = fma(-dm, ka, 1.0);
+    // center on the mean rounded to fp64, as the reference computes it
+    // (SPEC.md:127); (Kc + dm) - Kc is exact.  The expansions of phase B use
+    // the same (aa, ka), so they stay consistent.
+    const double aa = fma(-((Kc + dm) - Kc), ka, 1.0);
     if (lane == 0) {
       cb->bca.ka = ka;
       cb->bca.aa = aa;

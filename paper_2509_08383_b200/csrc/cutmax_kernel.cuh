@@ -569,6 +569,11 @@ __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, c
   // scalar chain of iteration t from (kcur, dm, s2): status, 1/sigma, k, b
   auto chain = [&](int t, double& kd, double& bd) {
     const double mu = kcur + dm;
+    // Center the input iteration on the fp64 mean, as the reference computes it
+    // (SPEC.md:127): mu is rounded to the double grid of the logits, and
+    // mu - kcur is exact (Sterbenz).  For rows whose |mean| / sigma is huge
+    // (e.g. 1e9 + N(0, 1e-2)) that rounding, not the summation, sets the result.
+    if (t == 0) dm = mu - kcur;
     // status: first failure wins (branch-free on the common path)
     const bool bad_range = !isfinite(mu) || !isfinite(s2);
     st = (st != PAM_OK) ? st : (bad_range ? PAM_ERR_RANGE : (s2 < eps_var ? PAM_ERR_DEGENERATE_INPUT : PAM_OK));
@@ -934,6 +939,10 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       // scalar chain of iteration t (+ the analytic normaliser for the last one)
       auto chain = [&](int t, double& kd, double& bd, double& rnorm) {
         const double mu = kcur + dm;
+        // input iteration: center on the reference's fp64-rounded mean (see the
+        // generic chain); T = 1 keeps dm, because its analytic normaliser uses
+        // the moments about dm
+        if (t == 0 && T > 1) dm = mu - kcur;
         const bool bad_range = !isfinite(mu) || !isfinite(s2);
         st = (st != PAM_OK) ? st : (bad_range ? PAM_ERR_RANGE : (s2 < eps_var ? PAM_ERR_DEGENERATE_INPUT : PAM_OK));
         if (stats_row) {
