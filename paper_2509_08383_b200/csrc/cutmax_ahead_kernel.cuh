@@ -328,6 +328,11 @@ __device__ __forceinline__ AhCoefB ah_phase_b_t(const double (&S)[10], const AhC
       }
     }
   }
+#ifdef PAM_AHEAD_NOCOND  // dev experiment: the cost of the condition bounds (unsafe; never shipped)
+  A3 = fabs(E3);
+  A6 = fabs(E6);
+  A9 = fabs(E9);
+#endif
   E3 *= inv_n;
   E6 *= inv_n;
   E9 *= inv_n;
