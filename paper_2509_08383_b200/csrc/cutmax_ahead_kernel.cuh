@@ -25,7 +25,7 @@
 //     -> [exchange] -> last pass: y4, y5 = Y, Z = Y / sum Y, argmax, and the
 //     next row's input moments (its X already sits in the row buffer).
 // Two exchanges per row instead of four, at 36 fp64 instructions per element
-// instead of 23 — the fp64 pipe was 37% busy, so the trade pays.
+// instead of 23 (the fp64 pipe is ~38% busy in cutmax_rows_kernel).
 //
 // Numerics.  The expansions are exact algebra; their rounding is bounded by
 // the condition number A_m / |E_m| (A_m the same sum over |terms|, with
@@ -39,10 +39,15 @@
 // condition numbers up to 2e3; the fallback almost never runs.
 //
 // Data movement.  The input row X(r+1) is TMA-loaded into the shared row
-// buffer during row r; the last pass of row r stores Z(r) straight from
-// registers (st.global.cs.v2, coalesced) while swapping X(r+1) - K0 into
-// registers, so the buffer is free at the row boundary and X(r+2) is loaded a
-// whole row period ahead.
+// buffer during row r.  The last pass of row r swaps it into registers and
+// writes Z(r) into the same slots; Z(r) leaves through 1-D TMA bulk stores
+// (tail-independent groups), and X(r+2) is loaded behind them at row r+1's
+// first mid exchange.  (Storing Z with st.global from registers instead queued
+// the exchanges' st.async behind 136 KB of stores.)
+//
+// Status: correct and opt-in (PAM_ENABLE_AHEAD); 50% of HBM at 4096 x 151936
+// vs 57% for cutmax_rows_kernel — the per-stage control path (wait, phase A,
+// phase B) runs from a cold instruction cache (DESIGN.md §4 K1b).
 //
 // Exchange.  Every thread writes its M partial sums to smem (part[j][tid]);
 // after one CTA barrier, warp j reduces column j (16 values per lane + a
