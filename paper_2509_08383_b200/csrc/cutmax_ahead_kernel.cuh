@@ -41,7 +41,7 @@
 // Data movement.  The input row X(r+1) is TMA-loaded into the shared row
 // buffer during row r.  The last pass of row r swaps it into registers and
 // writes Z(r) into the same slots; Z(r) leaves through 1-D TMA bulk stores
-// (tail-independent groups), and X(r+2) is loaded behind them at row r+1's
+// (4 bulk groups), and X(r+2) is loaded behind them at row r+1's
 // first mid exchange.  (Storing Z with st.global from registers instead queued
 // the exchanges' st.async behind 136 KB of stores.)
 //
