@@ -104,13 +104,24 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     }
     // Noise first (independent of x), then wait for the data.
     const uint64_t key = a.seed ^ (uint64_t)row;
+    if (GUMBEL || a.inv_alpha <= 19.0) {  // branch-free forms (bit-identical on this domain)
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const int li0 = (k * NT + tid) * VEC;
-      double u0, u1;
-      uniform_pair(key, a.draw, (uint64_t)(base + li0) >> 1, &u0, &u1);
-      v[k * VEC + 0] = GUMBEL ? gumbel_from_u(u0) : beta_icdf(u0, a.inv_alpha);
-      v[k * VEC + 1] = GUMBEL ? gumbel_from_u(u1) : beta_icdf(u1, a.inv_alpha);
+      for (int k = 0; k < NV; ++k) {
+        const int li0 = (k * NT + tid) * VEC;
+        double u0, u1;
+        uniform_pair(key, a.draw, (uint64_t)(base + li0) >> 1, &u0, &u1);
+        v[k * VEC + 0] = GUMBEL ? gumbel_fast(u0) : beta_icdf_fast(u0, a.inv_alpha);
+        v[k * VEC + 1] = GUMBEL ? gumbel_fast(u1) : beta_icdf_fast(u1, a.inv_alpha);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int li0 = (k * NT + tid) * VEC;
+        double u0, u1;
+        uniform_pair(key, a.draw, (uint64_t)(base + li0) >> 1, &u0, &u1);
+        v[k * VEC + 0] = GUMBEL ? gumbel_from_u(u0) : beta_icdf(u0, a.inv_alpha);
+        v[k * VEC + 1] = GUMBEL ? gumbel_from_u(u1) : beta_icdf(u1, a.inv_alpha);
+      }
     }
     PAM_TRACE(tr, 1);
     if (a.tma) {
@@ -247,7 +258,10 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
       for (int j = 0; j < VEC; ++j) {
         if (li0 + j < len) {
           const double xv = buf[li0 + j];
-          const double e = exp_p(xv - xmax);
+          // exp(x - max) for x - max >= -700 (bit-identical branch-free form); below,
+          // exp < 1e-304 cannot change the totals, which include exp(0) = 1
+          const double d = xv - xmax;
+          const double e = d >= -700.0 ? pam_exp_fast(d) : (d == d ? 0.0 : d);
           tot += e;
           if (xv > bestx) above += e;
         }

@@ -284,6 +284,88 @@ PAM_HD double beta_icdf(double u, double inv_alpha) {
 // Gumbel from uniform -log(-log u), u in (0,1).
 PAM_HD double gumbel_from_u(double u) { return -log_p(-log_p(u)); }
 
+#ifdef __CUDACC__
+// ---- branch-free device forms of the above, bit-identical on their domain ----
+// The portable functions branch per element on special cases (NaN, 0, inf,
+// subnormal, overflow) and divide with div.rn.f64, whose slow-path call splits
+// the sampler's unrolled noise loop into one basic block per element (no
+// cross-element ILP).  On the inputs the sampler feeds them, none of the special
+// cases can occur, and these forms run the same arithmetic without branches.
+// tools/fastmath_check.cu compares them bit for bit with the portable forms.
+
+// Correctly rounded a / b for b in [1.7, 2.5], |a| < 1: the div.rn.f64 fast
+// path (reciprocal estimate, two Newton steps, one FMA correction) without its
+// exponent-range checks, which cannot trigger on this range.
+__device__ __forceinline__ double pam_div_nr(double a, double b) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+  double e = fma(-b, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-b, y, 1.0);
+  y = fma(y, e, y);
+  const double q = a * y;
+  const double r = fma(-b, q, a);
+  return fma(r, y, q);
+}
+
+// log_p for positive normal finite x.
+__device__ __forceinline__ double pam_log_fast(double x) {
+  const uint64_t xb = pam_double_to_bits(x);
+  int e = (int)(xb >> 52) - 1022;
+  double m = pam_bits_to_double((xb & 0x000fffffffffffffULL) | 0x3fe0000000000000ULL);
+  const bool lo = m < 0x1.6a09e667f3bcdp-1;
+  m = lo ? m + m : m;
+  e = lo ? e - 1 : e;
+  const double f = pam_div_nr(m - 1.0, m + 1.0);
+  const double s = f * f;
+  double q = 0x1.642c8590b2164p-5;
+  q = fma(q, s, 0x1.8618618618618p-5);
+  q = fma(q, s, 0x1.af286bca1af28p-5);
+  q = fma(q, s, 0x1.e1e1e1e1e1e1ep-5);
+  q = fma(q, s, 0x1.1111111111111p-4);
+  q = fma(q, s, 0x1.3b13b13b13b14p-4);
+  q = fma(q, s, 0x1.745d1745d1746p-4);
+  q = fma(q, s, 0x1.c71c71c71c71cp-4);
+  q = fma(q, s, 0x1.2492492492492p-3);
+  q = fma(q, s, 0x1.999999999999ap-3);
+  q = fma(q, s, 0x1.5555555555555p-2);
+  const double t = f + f;
+  const double logm = fma(t * s, q, t);
+  const double ed = (double)e;
+  return fma(ed, 0x1.62e42fefa3800p-1, fma(ed, 0x1.ef35793c76730p-45, logm));
+}
+
+// exp_p for -700 <= x <= 709 (k = rint(x / ln2) in [-1010, 1023]: no flush, no overflow).
+__device__ __forceinline__ double pam_exp_fast(double x) {
+  const double k = rint(x * 0x1.71547652b82fep+0);
+  double r = fma(-k, 0x1.62e42fefa3800p-1, x);
+  r = fma(-k, 0x1.ef35793c76730p-45, r);
+  double p = 0x1.6124613a86d09p-33;
+  p = fma(p, r, 0x1.1eed8eff8d898p-29);
+  p = fma(p, r, 0x1.ae64567f544e4p-26);
+  p = fma(p, r, 0x1.27e4fb7789f5cp-22);
+  p = fma(p, r, 0x1.71de3a556c734p-19);
+  p = fma(p, r, 0x1.a01a01a01a01ap-16);
+  p = fma(p, r, 0x1.a01a01a01a01ap-13);
+  p = fma(p, r, 0x1.6c16c16c16c17p-10);
+  p = fma(p, r, 0x1.1111111111111p-7);
+  p = fma(p, r, 0x1.5555555555555p-5);
+  p = fma(p, r, 0x1.5555555555555p-3);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  return p * pam_pow2((int)k);
+}
+
+// beta_icdf for u in [2^-53, 1 - 2^-53] (u01_from_bits) and inv_alpha <= 19
+// (then log(u) * inv_alpha >= -700); callers check inv_alpha once per launch.
+__device__ __forceinline__ double beta_icdf_fast(double u, double inv_alpha) {
+  return inv_alpha == 1.0 ? u : pam_exp_fast(pam_log_fast(u) * inv_alpha);
+}
+// gumbel_from_u for u in [2^-53, 1 - 2^-53].
+__device__ __forceinline__ double gumbel_fast(double u) { return -pam_log_fast(-pam_log_fast(u)); }
+#endif
+
 }  // namespace pam
 
 #endif  // PAM_SCALAR_H
