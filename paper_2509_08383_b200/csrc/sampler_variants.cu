@@ -14,7 +14,8 @@ namespace pam {
 
 const SamplerVariant kSamplerVariants[] = {
     PAM_SAMPLER_VARIANT(64, 2),   PAM_SAMPLER_VARIANT(128, 8),  PAM_SAMPLER_VARIANT(256, 8),
-    PAM_SAMPLER_VARIANT(256, 16), PAM_SAMPLER_VARIANT(512, 16), PAM_SAMPLER_VARIANT(512, 24),
+    PAM_SAMPLER_VARIANT(256, 16), PAM_SAMPLER_VARIANT(512, 16), PAM_SAMPLER_VARIANT(512, 20),
+    PAM_SAMPLER_VARIANT(512, 24), PAM_SAMPLER_VARIANT(512, 32),  // exact fits: n = 16 x 9496+, 2 x 16384
     PAM_SAMPLER_VARIANT(512, 38),
 };
 const int kNumSamplerVariants = sizeof(kSamplerVariants) / sizeof(kSamplerVariants[0]);
