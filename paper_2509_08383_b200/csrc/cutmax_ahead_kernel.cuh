@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_ahead_kernel(const CutmaxArgs a
   // Sl: lane l holds S_{l+1} of the stage iterate (shifted by Kc).  Publishes
   // (ka, aa) so the other warps can run the first half of the pass while
   // phase B (the expansions) is still computing.
-  auto phase_a = [&](int i, double Sl, double Kc, int st, double& dm_out) {
+  auto phase_a = [&](int i, double Sl, double Kc, int st) {
     const int it = 2 * i;
     const double S1 = __shfl_sync(FULL, Sl, 0), S2 = __shfl_sync(FULL, Sl, 1);
     if (i == 0 && st == PAM_OK && (!isfinite(S1) || !isfinite(S2))) st = PAM_ERR_NON_FINITE;
@@ -598,7 +598,6 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_ahead_kernel(const CutmaxArgs a
       cb->kc = Kc;
     }
     __syncwarp();  // (warp 0 itself reads kc in the exact path)
-    dm_out = dm;
     return AhCoefA{ka, aa, st, slow ? 1 : 0};
   };
   // ---- control warp, phase B: iteration s+1 and the normaliser ----------------
@@ -813,8 +812,7 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_ahead_kernel(const CutmaxArgs a
           if (a.status) a.status[row_prev] = st_prev;
         }
         const double Kc = (i == 0) ? K0 : rp.kshift[2 * i];
-        double dm;
-        ca = phase_a(i, Sl, Kc, st, dm);
+        ca = phase_a(i, Sl, Kc, st);
         PAM_TRACE(tr, i == 0 ? 2 : 15);
         bar2_arrive();
       } else {
