@@ -552,3 +552,18 @@ def test_random_shapes_and_params(cuda, pam, orc, kernel):
             check_rows(z, am, st, zr, amr, str_, tol)
     finally:
         os.environ.pop("PAM_ENABLE_AHEAD", None)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_host_entry_multi_chunk(cuda, pam, orc, dtype):
+    """Host-buffer C ABI with 1 MiB pipeline chunks (PAM_HOST_CHUNK_MB): many
+    chunks over the 3 streams plus a partial last chunk, fp64 and fp32."""
+    x = W.gaussian(37, 32768, seed=91).astype(dtype)  # 256 KiB (fp64) rows: 4 per chunk, last one partial
+    prm = pam.CutMaxParams()
+    os.environ["PAM_HOST_CHUNK_MB"] = "1"
+    try:
+        z, am, st = pam.cutmax_batch(x, prm, raise_on_error=False)
+    finally:
+        del os.environ["PAM_HOST_CHUNK_MB"]
+    zr, amr, str_ = orc.cutmax_batch(x, prm.lower())
+    check_rows(np.asarray(z), np.asarray(am), np.asarray(st), zr, amr, str_, TOL64 if dtype == np.float64 else TOL32)
