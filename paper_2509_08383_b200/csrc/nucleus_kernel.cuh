@@ -105,13 +105,28 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     // Noise first (independent of x), then wait for the data.
     const uint64_t key = a.seed ^ (uint64_t)row;
     if (GUMBEL || a.inv_alpha <= 19.0) {  // branch-free forms (bit-identical on this domain)
+      // two vector slots (four elements) per step, their chains written side by
+      // side so the scheduler keeps four independent log/exp chains in flight
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int li0 = (k * NT + tid) * VEC;
-        double u0, u1;
-        uniform_pair(key, a.draw, (uint64_t)(base + li0) >> 1, &u0, &u1);
-        v[k * VEC + 0] = GUMBEL ? gumbel_fast(u0) : beta_icdf_fast(u0, a.inv_alpha);
-        v[k * VEC + 1] = GUMBEL ? gumbel_fast(u1) : beta_icdf_fast(u1, a.inv_alpha);
+      for (int k = 0; k < NV; k += 2) {
+        const int k1 = k + 1 < NV ? k + 1 : k;
+        const int li0 = (k * NT + tid) * VEC, li1 = (k1 * NT + tid) * VEC;
+        double u[4];
+        uniform_pair(key, a.draw, (uint64_t)(base + li0) >> 1, &u[0], &u[1]);
+        uniform_pair(key, a.draw, (uint64_t)(base + li1) >> 1, &u[2], &u[3]);
+        double g[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) g[q] = GUMBEL ? -pam_log_fast(u[q]) : pam_log_fast(u[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) g[q] = GUMBEL ? -pam_log_fast(g[q]) : pam_exp_fast(g[q] * a.inv_alpha);
+        if (!GUMBEL && a.inv_alpha == 1.0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) g[q] = u[q];
+        }
+        v[k * VEC + 0] = g[0];
+        v[k * VEC + 1] = g[1];
+        v[k1 * VEC + 0] = g[2];
+        v[k1 * VEC + 1] = g[3];
       }
     } else {
 #pragma unroll
