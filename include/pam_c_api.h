@@ -61,8 +61,10 @@ typedef enum pam_status {
   PAM_ERR_SINGULAR = 10         /* SingularityError     (errors.hpp:55): JVP through s^2 < eps_var */
 } pam_status;
 
-/* Row flag bits OR-ed into the per-row status value's high byte (never an error). */
-#define PAM_ROW_FLAG_TIE 0x100      /* TieWarning: input top-2 gap < 1e-9 */
+/* Row flag bits OR-ed into the per-row status value's high byte (never an error;
+ * test errors with (status & 0xff) != PAM_OK).  Set only on PAM_OK rows. */
+#define PAM_ROW_FLAG_TIE 0x100      /* TieWarning: input top-2 gap < 1e-9; the
+                                       sampler tests x + G, the vector CutMax sees */
 
 /* ApproxConfig.  `rescale` selects how the caller-side
  * rescaling of SPEC.md:205 / PAPER.md:139 is done:
@@ -92,7 +94,9 @@ enum { PAM_MODE_EXACT = 0, PAM_MODE_POLY = 1 };
 
 /* CutMaxParams with the decisions of SPEC.md:121-127:
  * per-iteration schedules p[t], c[t] for t < T (scalars are broadcast by the
- * C++/Python front ends), eps_var (default 1e-24), eps_stop (0 = off). */
+ * C++/Python front ends), eps_var (default 1e-24), eps_stop (0 = off; > 0 stops
+ * after iteration t < T-1 once max Y / sum Y >= 1 - eps_stop, SPEC.md:126 —
+ * CutMax f64/f32 and both samplers; the analysis entry points reject it). */
 typedef struct pam_cutmax_params {
   int32_t T;
   int32_t flags;
@@ -218,6 +222,16 @@ int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_par
                      pam_launch_info* info);
 /* Number of kernels this library launched since load (tests / bench evidence). */
 int64_t pam_kernel_launch_count(void);
+/* Tuning / test hooks (explicit calls; the library reads no environment variables).
+ * pam_set_geometry_override: force the CutMax geometry for one dtype (threads x
+ *   elems_per_thread per CTA from the compiled variant table, cluster size 1..16,
+ *   launch-bounds min_blocks); threads = 0 clears it.  PAM_ERR_UNSUPPORTED if no
+ *   such variant is compiled.  A forced geometry that cannot hold a row makes the
+ *   batch call return PAM_ERR_UNSUPPORTED.
+ * pam_set_host_chunk_bytes: pipeline chunk of the host-pointer entry points
+ *   (default 128 MiB of input per chunk; <= 0 restores the default). */
+int pam_set_geometry_override(int dtype_bytes, int threads, int elems_per_thread, int cluster, int min_blocks);
+int pam_set_host_chunk_bytes(int64_t bytes);
 /* Debug: device buffer (grid x 8 rows x 32 events of int64 clock64 stamps) that
  * the CutMax kernel fills with per-CTA phase timestamps; NULL disables. */
 void pam_set_trace_buffer(long long* d_buf, int64_t entries);

@@ -65,11 +65,13 @@ struct CutMaxParams {
   pam_cutmax_params lower() const;
 };
 
-/// ScoreVector plus the argmax the kernel computes anyway.
+/// ScoreVector plus the argmax the kernel computes anyway and
+/// the TieWarning (input top-2 gap < 1e-9; reported, not thrown).
 struct ScoreVector {
   std::vector<double> values;
   bool normalized = true;
   int argmax = -1;
+  bool tieWarning = false;
 };
 
 /// ResidualStats.
@@ -88,11 +90,12 @@ struct SamplerConfig {
   std::uint64_t draw = 0;
 };
 
-/// SampleOutcome.
+/// SampleOutcome plus the TieWarning of the perturbed vector x + G.
 struct SampleOutcome {
   std::vector<double> onehot;
   int tokenIndex = -1;
   bool insideNucleus = false;
+  bool tieWarning = false;
 };
 
 // ---- single-vector API (host vectors; GPU underneath) ----------------------

@@ -304,7 +304,20 @@ int orc_cutmax(const double* x, int64_t n, const pam_cutmax_params* prm,
     for (i = 0; i < n; ++i) z[i] = z[i] * r;                    /* PAPER.md:69 / :163 */
   }
   if (argmax) *argmax = (int32_t)best;
-  return PAM_OK;
+  return orc_tie_warning(x, n);                                 /* PAM_OK | TieWarning flag */
+}
+
+/* TieWarning on an fp32 input: the top-2 gap of the float values, taken in
+ * fp64 (exact: the difference of two floats fits a double). */
+static int orc_tie_warning_f32(const float* x, int64_t n) {
+  double m1 = -INFINITY, m2 = -INFINITY;
+  int64_t i;
+  for (i = 0; i < n; ++i) {
+    double v = (double)x[i];
+    if (v > m1) { m2 = m1; m1 = v; }
+    else if (v > m2) m2 = v;
+  }
+  return (m1 - m2 < 1e-9) ? PAM_ROW_FLAG_TIE : 0;
 }
 
 /* fp32 path: fp32 storage and elementwise math, fp64 statistics and scalars. */
@@ -315,7 +328,6 @@ int orc_cutmax_f32(const float* x, int64_t n, const pam_cutmax_params* prm,
   int t;
   if (argmax) *argmax = -1;
   if (st) return st;
-  if (prm->eps_stop > 0.0) return PAM_ERR_UNSUPPORTED;
   for (i = 0; i < n; ++i)
     if (!isfinite(x[i])) return PAM_ERR_NON_FINITE;
   for (i = 0; i < n; ++i) z[i] = x[i];
@@ -343,6 +355,11 @@ int orc_cutmax_f32(const float* x, int64_t n, const pam_cutmax_params* prm,
       float u = (z[i] - muf) * kf + 1.0f;
       z[i] = orc_ipowf(u, p);
     }
+    if (prm->eps_stop > 0.0 && t + 1 < prm->T) {                 /* SPEC.md:126, as the fp64 path */
+      double s = 0.0, m = -INFINITY;
+      for (i = 0; i < n; ++i) { s += (double)z[i]; if ((double)z[i] > m) m = (double)z[i]; }
+      if (m / s >= 1.0 - prm->eps_stop) break;
+    }
   }
   int64_t best = 0;
   for (i = 1; i < n; ++i) if (z[i] > z[best]) best = i;        /* argmax of Y^(T+1), pin A7 */
@@ -362,7 +379,7 @@ int orc_cutmax_f32(const float* x, int64_t n, const pam_cutmax_params* prm,
     for (i = 0; i < n; ++i) z[i] = z[i] * rf;
   }
   if (argmax) *argmax = (int32_t)best;
-  return PAM_OK;
+  return orc_tie_warning_f32(x, n);
 }
 
 int64_t orc_cutmax_batch(const double* x, int64_t ld, int64_t B, int64_t n,
@@ -378,7 +395,7 @@ int64_t orc_cutmax_batch(const double* x, int64_t ld, int64_t B, int64_t n,
     int st = orc_cutmax(x + r * ld, n, prm, z + r * ldz, &am, NULL, NULL);
     if (argmax) argmax[r] = am;
     if (status) status[r] = st;
-    if (st) bad++;
+    if (st & 0xff) bad++;                                       /* the TieWarning bit is not a failure */
   }
   (void)nthreads;
   return bad;
@@ -397,7 +414,7 @@ int64_t orc_cutmax_batch_f32(const float* x, int64_t ld, int64_t B, int64_t n,
     int st = orc_cutmax_f32(x + r * ld, n, prm, z + r * ldz, &am, NULL);
     if (argmax) argmax[r] = am;
     if (status) status[r] = st;
-    if (st) bad++;
+    if (st & 0xff) bad++;                                       /* the TieWarning bit is not a failure */
   }
   (void)nthreads;
   return bad;
@@ -590,8 +607,8 @@ int orc_sample(const double* x, int64_t n, const pam_sampler_cfg* cfg, const pam
     xt[i] = x[i] + g;                                                  /* line 5 */
   }
   int32_t am = -1;
-  int st = orc_cutmax(xt, n, prm, zz, &am, NULL, NULL);                /* line 6 */
-  if (st == PAM_OK) {
+  int st = orc_cutmax(xt, n, prm, zz, &am, NULL, NULL);                /* line 6; TieWarning on x~ */
+  if ((st & 0xff) == PAM_OK) {
     *token = am;
     *inside = (uint8_t)orc_nucleus_inside(x, n, cfg->p, am);
   }
@@ -611,7 +628,7 @@ int64_t orc_sample_batch(const double* x, int64_t ld, int64_t B, int64_t n, cons
   for (r = 0; r < B; ++r) {
     int st = orc_sample(x + r * ld, n, cfg, prm, (uint64_t)r, gumbel, &token[r], &inside[r], NULL);
     if (status) status[r] = st;
-    if (st) bad++;
+    if (st & 0xff) bad++;                                       /* the TieWarning bit is not a failure */
   }
   (void)nthreads;
   return bad;

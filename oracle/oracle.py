@@ -12,7 +12,65 @@ import subprocess
 
 import numpy as np
 
-from paper_2509_08383_b200 import _abi  # struct layouts of include/pam_c_api.h (types only)
+
+class _abi:
+    """ctypes restatement of the struct layouts in include/pam_c_api.h.
+
+    Defined here, not imported from the product package, so loading the oracle
+    never maps libpam.so (bench.py --impl reference must not touch the product).
+    tests/test_abi.py checks these layouts against the product's _abi.py."""
+
+    PAM_MAX_T = 16
+    PAM_MODE_EXACT, PAM_MODE_POLY = 0, 1
+    PAM_RESCALE_AUTO, PAM_RESCALE_STATIC, PAM_RESCALE_NONE = 0, 1, 2
+    PAM_ROW_FLAG_TIE = 0x100
+
+    class pam_approx_config(C.Structure):
+        _fields_ = [("iterations", C.c_int32), ("alpha_bits", C.c_int32), ("rescale", C.c_int32),
+                    ("scale_log2", C.c_int32), ("lo", C.c_double), ("hi", C.c_double)]
+
+    class pam_cutmax_params(C.Structure):
+        pass
+
+    class pam_sampler_cfg(C.Structure):
+        _fields_ = [("p", C.c_double), ("q", C.c_double), ("alpha", C.c_double), ("seed", C.c_uint64),
+                    ("draw", C.c_uint64)]
+
+
+_abi.pam_cutmax_params._fields_ = [
+    ("T", C.c_int32), ("flags", C.c_int32), ("invsqrt_mode", C.c_int32), ("inv_mode", C.c_int32),
+    ("p", C.c_int32 * _abi.PAM_MAX_T), ("c", C.c_double * _abi.PAM_MAX_T), ("eps_var", C.c_double),
+    ("eps_stop", C.c_double), ("invsqrt", _abi.pam_approx_config * _abi.PAM_MAX_T),
+    ("inv", _abi.pam_approx_config)]
+
+
+def default_params(T: int = 4, p: int = 3, c: float = 5.0, eps_stop: float = 0.0) -> "_abi.pam_cutmax_params":
+    """CutMaxParams defaults: p, c broadcast over T,
+    eps_var = 1e-24, exact 1/sqrt and 1/S, invsqrt preset alpha=7 (5 Newton
+    iterations, Table 3), Goldschmidt d=5, AUTO rescale.  Same
+    values as the product's pam_default_params (checked by tests/test_abi.py)."""
+    r = _abi.pam_cutmax_params()
+    r.T = int(T)
+    r.eps_var = 1e-24
+    r.eps_stop = float(eps_stop)
+    r.invsqrt_mode = _abi.PAM_MODE_EXACT
+    r.inv_mode = _abi.PAM_MODE_EXACT
+    for t in range(_abi.PAM_MAX_T):
+        r.p[t] = int(p)
+        r.c[t] = float(c)
+        a = r.invsqrt[t]
+        a.iterations, a.alpha_bits, a.rescale, a.lo, a.hi = 5, 7, _abi.PAM_RESCALE_AUTO, 0.25, 1.0
+    r.inv.iterations, r.inv.alpha_bits, r.inv.rescale, r.inv.lo, r.inv.hi = 5, 7, _abi.PAM_RESCALE_AUTO, 0.5, 1.0
+    return r
+
+
+def _as(struct_type, v):
+    """Accept the product's ctypes structs too (same layout, different class):
+    tests lower parameters with the product's front end and hand them here."""
+    if v is None or isinstance(v, struct_type):
+        return v
+    return struct_type.from_buffer_copy(bytes(memoryview(v)))
+
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
@@ -82,7 +140,7 @@ def cutmax(x, prm: _abi.pam_cutmax_params):
     z = np.empty(n)
     am = C.c_int32(-1)
     stats = np.zeros((prm.T, 2))
-    st = lib.orc_cutmax(x.ctypes.data, n, C.byref(prm), z.ctypes.data, C.byref(am), stats.ctypes.data, None)
+    st = lib.orc_cutmax(x.ctypes.data, n, C.byref(_as(_abi.pam_cutmax_params, prm)), z.ctypes.data, C.byref(am), stats.ctypes.data, None)
     return st, z, am.value, stats
 
 
@@ -100,7 +158,7 @@ def cutmax_batch(X, prm, nthreads: int = 0):
     z = np.empty_like(X)
     am = np.empty(B, dtype=np.int32)
     st = np.empty(B, dtype=np.int32)
-    fn(X.ctypes.data, n, B, n, C.byref(prm), z.ctypes.data, n, am.ctypes.data, st.ctypes.data, nthreads)
+    fn(X.ctypes.data, n, B, n, C.byref(_as(_abi.pam_cutmax_params, prm)), z.ctypes.data, n, am.ctypes.data, st.ctypes.data, nthreads)
     return z, am, st
 
 
@@ -112,7 +170,7 @@ def sample_batch(X, cfg: _abi.pam_sampler_cfg, prm, gumbel: bool = False, nthrea
     tok = np.empty(B, dtype=np.int32)
     ins = np.empty(B, dtype=np.uint8)
     st = np.empty(B, dtype=np.int32)
-    lib.orc_sample_batch(X.ctypes.data, n, B, n, C.byref(cfg), C.byref(prm), int(gumbel), tok.ctypes.data,
+    lib.orc_sample_batch(X.ctypes.data, n, B, n, C.byref(_as(_abi.pam_sampler_cfg, cfg)), C.byref(_as(_abi.pam_cutmax_params, prm)), int(gumbel), tok.ctypes.data,
                          ins.ctypes.data, st.ctypes.data, nthreads)
     return tok, ins, st
 
@@ -151,7 +209,7 @@ def contraction_factor(n: int, p: int, c: float):
 def convergence_trace(x, prm):
     x = _f64(x)
     out = np.zeros((prm.T, 4))
-    st = load().orc_convergence_trace(x.ctypes.data, x.shape[0], C.byref(prm), out.ctypes.data)
+    st = load().orc_convergence_trace(x.ctypes.data, x.shape[0], C.byref(_as(_abi.pam_cutmax_params, prm)), out.ctypes.data)
     return st, out
 
 
@@ -161,7 +219,7 @@ def cutmax_jvp(x, v, prm):
     v = _f64(v)
     z = np.empty_like(x)
     dz = np.empty_like(x)
-    st = load().orc_cutmax_jvp(x.ctypes.data, v.ctypes.data, x.shape[0], C.byref(prm), z.ctypes.data, dz.ctypes.data)
+    st = load().orc_cutmax_jvp(x.ctypes.data, v.ctypes.data, x.shape[0], C.byref(_as(_abi.pam_cutmax_params, prm)), z.ctypes.data, dz.ctypes.data)
     return st, z, dz
 
 
@@ -185,5 +243,5 @@ def scalar(name: str, *args):
 def approx_cfg(x: float, cfg: _abi.pam_approx_config, inv: bool):
     out = C.c_double()
     fn = load().orc_inv_cfg if inv else load().orc_invsqrt_cfg
-    st = fn(x, C.byref(cfg), C.byref(out))
+    st = fn(x, C.byref(_as(_abi.pam_approx_config, cfg)), C.byref(out))
     return st, out.value

@@ -62,6 +62,7 @@ struct RowParams {
   double inv_c[PAM_MAX_T];
   double kshift[PAM_MAX_T + 1];  // shift of the stored Y^(t+1) values; kshift[T] = 0
   double eps_var;
+  double eps_stop;  // early stop when max Y / sum Y >= 1 - eps_stop; 0 = off (generic flow only)
   pam_approx_config invsqrt[PAM_MAX_T];
   pam_approx_config inv;
 };
@@ -76,7 +77,6 @@ struct CutmaxArgs {
   int32_t L;            // slice length per CTA (elements)
   int32_t ctrl_offset;  // byte offset of the control block (after the row buffer)
   int32_t tma;          // 1: TMA bulk loads/stores (16-byte aligned rows), 0: direct loads/stores
-  int32_t debug_flags;  // dev experiments: 1 = skip Z stores
   double inv_n;         // 1/n
   long long* trace;     // debug: per-CTA phase timestamps (pam_set_trace_buffer), normally null
   RowParams rp;
@@ -87,15 +87,6 @@ struct CutmaxArgs {
 struct __align__(16) XchRecord {
   double2 ab;
   double2 cand;  // (value, index bits)
-};
-
-// One exchange channel (the dual-row kernel runs two; ControlBlock embeds the
-// same members so the exchange templates take either).
-struct __align__(16) XchChannel {
-  XchRecord xch[2][16];  // slots per cluster rank, double-buffered by round parity
-  double2 wred[32];      // per-warp partial sums
-  double2 wcand[32];     // per-warp argmax candidates / third sums
-  unsigned long long mb_x[2];
 };
 
 // Coefficients the control warp publishes for the next pass (p = 3 flow).
@@ -114,6 +105,9 @@ struct __align__(16) ControlBlock {
   double2 wcand[32];     // per-warp argmax candidates
   double2 wred2[32];     // per-warp partials of the next row's input sums
   double2 gat[16][2];    // all-gather records (sampler: token candidate + max x)
+  double2 tin[2][16];    // input top-2 records (TieWarning) per cluster rank, by local row parity
+  double2 wt2[32];       // per-warp top-2 partials
+  unsigned long long mb_t[2];
   unsigned long long mb_load;
   unsigned long long mb_x[2];
   unsigned long long mb_g;
@@ -215,6 +209,62 @@ __device__ __forceinline__ void bfly_argmax(double& best, long long& besti) {
 }
 
 // ---------------------------------------------------------------------------
+// Input top-2 (TieWarning: the top-2 gap of the input < 1e-9).
+// (m1, m2) = the largest and second-largest entry of the multiset (a
+// duplicated maximum gives m2 = m1), exactly as the oracle's orc_tie_warning.
+// min/max are exact and commutative, so every merge order gives the same pair.
+__device__ __forceinline__ double emax(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ double emin(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ float emax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ float emin(float a, float b) { return fminf(a, b); }
+template <typename Elem>
+__device__ __forceinline__ void top2_add(Elem& m1, Elem& m2, Elem x) {
+  m2 = emax(m2, emin(m1, x));
+  m1 = emax(m1, x);
+}
+__device__ __forceinline__ void top2_merge(double& a1, double& a2, double b1, double b2) {
+  a2 = fmax(fmin(a1, b1), fmax(a2, b2));
+  a1 = fmax(a1, b1);
+}
+template <int WIDTH>
+__device__ __forceinline__ void bfly_top2(double& a1, double& a2) {
+#pragma unroll
+  for (int m = WIDTH / 2; m > 0; m >>= 1) {
+    const double b1 = __shfl_xor_sync(0xffffffffu, a1, m), b2 = __shfl_xor_sync(0xffffffffu, a2, m);
+    top2_merge(a1, a2, b1, b2);
+  }
+}
+__device__ __forceinline__ int tie_flag(int st, double2 t) {
+  return (st == PAM_OK && t.x - t.y < 1e-9) ? PAM_ROW_FLAG_TIE : 0;
+}
+// Top-2 side record of an exchange: the CTA's pair, butterflied over each
+// warp, goes to slot `slot` (the row's local parity) of every CTA with its own
+// mbarrier mb_t[slot]; top2_wait (warp 0, at the row's status write) combines
+// the C records.  Exactly one record per row, so no phase is ever skipped.
+struct Top2Push {
+  bool on;
+  double m1, m2;
+  uint32_t slot;
+};
+__device__ __forceinline__ Top2Push no_top2() { return Top2Push{false, 0.0, 0.0, 0u}; }
+
+// `phases` holds the current mbarrier phase of slot s in bit s.
+__device__ __forceinline__ double2 top2_wait(ControlBlock* cb, const uint32_t slot, uint32_t& phases,
+                                             const uint32_t C, const int gtid) {
+  const int lane = gtid & 31;
+  ptx::mbar_wait_cta(ptx::smem_addr(&cb->mb_t[slot]), (phases >> slot) & 1u);
+  phases ^= 1u << slot;
+  const int src = lane & 15;
+  const bool have = src < (int)C;
+  const double2 rec = cb->tin[slot][have ? src : 0];
+  __syncwarp();
+  if (gtid == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[slot]), C * 16u);  // arm row + 2
+  double m1 = have ? rec.x : -HUGE_VAL, m2 = have ? rec.y : -HUGE_VAL;
+  bfly_top2<16>(m1, m2);
+  return make_double2(m1, m2);
+}
+
+// ---------------------------------------------------------------------------
 // Cluster exchange, split in two so independent work can run between the push
 // and the wait.  All NTG threads of the CTA call both halves.
 //
@@ -235,18 +285,19 @@ enum XchMode { kSum2 = 0, kSum3 = 1, kArgmax = 2 };
 template <int NTG, int MODE, typename Ch, typename Side = NoSide>
 __device__ __forceinline__ void xch_push(double a, double b, double c, long long ci_, Ch* cb,
                                          const uint32_t round, const uint32_t rank, const uint32_t C, const int gtid,
-                                         const Side& side = Side(), const bool third = true) {
+                                         const Side& side = Side(), const bool third = true,
+                                         Top2Push t2 = no_top2()) {
   constexpr int NW = NTG / 32;
   const int lane = gtid & 31, warp = gtid >> 5;
-  double c2 = 0.0;  // unused partner of c in kSum3 (keeps the butterfly a pair)
   long long ci = ci_;
   bfly_sum2<32>(a, b);
   if (MODE == kArgmax) bfly_argmax<32>(c, ci);
   if (MODE == kSum3 && third) bfly_sum1<32>(c);
-  (void)c2;
+  if (t2.on) bfly_top2<32>(t2.m1, t2.m2);
   if (lane == 0) {
     cb->wred[warp] = make_double2(a, b);
     if (MODE == kArgmax || (MODE == kSum3 && third)) cb->wcand[warp] = make_double2(c, __longlong_as_double(ci));
+    if (t2.on) cb->wt2[warp] = make_double2(t2.m1, t2.m2);
   }
   __syncthreads();
   const uint32_t par = round & 1u;
@@ -268,6 +319,14 @@ __device__ __forceinline__ void xch_push(double a, double b, double c, long long
       ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->xch[par][rank].ab), (uint32_t)lane), ca, cbv, bar);
       ptx::st_async_b64x2(ptx::mapa(ptx::smem_addr(&cb->xch[par][rank].cand), (uint32_t)lane),
                           (uint64_t)__double_as_longlong(cv), (uint64_t)cix, bar);
+    }
+    if (t2.on) {
+      const double2 w2 = cb->wt2[lane & (NW - 1)];
+      double m1 = w2.x, m2 = w2.y;
+      bfly_top2<NW>(m1, m2);
+      if (lane < (int)C)
+        ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->tin[t2.slot][rank]), (uint32_t)lane), m1, m2,
+                            ptx::mapa(ptx::smem_addr(&cb->mb_t[t2.slot]), (uint32_t)lane));
     }
   } else if (warp == NW - 1 && lane == 0) {
     side();
@@ -306,26 +365,28 @@ __device__ __forceinline__ double2 xch_wait(double& c, long long& ci, Ch* cb, ui
 template <int NTG, bool ARGMAX, typename Ch>
 __device__ __forceinline__ double2 cluster_reduce(double a, double b, double& best, long long& besti, Ch* cb,
                                                   uint32_t& round, const uint32_t rank, const uint32_t C,
-                                                  const int gtid) {
+                                                  const int gtid, Top2Push t2 = no_top2()) {
   constexpr int M = ARGMAX ? kArgmax : kSum2;
-  xch_push<NTG, M>(a, b, best, besti, cb, round, rank, C, gtid);
+  xch_push<NTG, M>(a, b, best, besti, cb, round, rank, C, gtid, NoSide(), true, t2);
   return xch_wait<M>(best, besti, cb, round, C, gtid);
 }
 
 template <int NTG, typename Ch>
 __device__ __forceinline__ double2 cluster_sum2(double a, double b, Ch* cb, uint32_t& round,
-                                                const uint32_t rank, const uint32_t C, const int gtid) {
+                                                const uint32_t rank, const uint32_t C, const int gtid,
+                                                Top2Push t2 = no_top2()) {
   double bv = 0.0;
   long long bi = 0;
-  return cluster_reduce<NTG, false>(a, b, bv, bi, cb, round, rank, C, gtid);
+  return cluster_reduce<NTG, false>(a, b, bv, bi, cb, round, rank, C, gtid, t2);
 }
 
 // Three cluster sums in one exchange.
 template <int NTG, typename Ch>
 __device__ __forceinline__ double3 cluster_sum3(double a, double b, double c, Ch* cb, uint32_t& round,
-                                                const uint32_t rank, const uint32_t C, const int gtid) {
+                                                const uint32_t rank, const uint32_t C, const int gtid,
+                                                Top2Push t2 = no_top2()) {
   long long ci = 0;
-  xch_push<NTG, kSum3>(a, b, c, ci, cb, round, rank, C, gtid);
+  xch_push<NTG, kSum3>(a, b, c, ci, cb, round, rank, C, gtid, NoSide(), true, t2);
   const double2 r = xch_wait<kSum3>(c, ci, cb, round, C, gtid);
   return make_double3(r.x, r.y, c);
 }
@@ -334,19 +395,28 @@ __device__ __forceinline__ double3 cluster_sum3(double a, double b, double c, Ch
 // slots, own records and mbarrier (mb_in, one phase per row).
 template <int NTG>
 __device__ __forceinline__ void xin_push(double s, double q, ControlBlock* cb, const uint32_t rank, const uint32_t C,
-                                         const int gtid) {
+                                         const int gtid, Top2Push t2) {
   constexpr int NW = NTG / 32;
   const int lane = gtid & 31, warp = gtid >> 5;
   bfly_sum2<32>(s, q);
-  if (lane == 0) cb->wred2[warp] = make_double2(s, q);
+  bfly_top2<32>(t2.m1, t2.m2);
+  if (lane == 0) {
+    cb->wred2[warp] = make_double2(s, q);
+    cb->wt2[warp] = make_double2(t2.m1, t2.m2);
+  }
   __syncthreads();
   if (warp == 0) {
     const double2 w = cb->wred2[lane & (NW - 1)];
     double cs = w.x, cq = w.y;
     bfly_sum2<NW>(cs, cq);
+    const double2 w2 = cb->wt2[lane & (NW - 1)];
+    double m1 = w2.x, m2 = w2.y;
+    bfly_top2<NW>(m1, m2);
     if (lane < (int)C) {
       const uint32_t bar = ptx::mapa(ptx::smem_addr(&cb->mb_in), (uint32_t)lane);
       ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->xin[rank]), (uint32_t)lane), cs, cq, bar);
+      ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->tin[t2.slot][rank]), (uint32_t)lane), m1, m2,
+                          ptx::mapa(ptx::smem_addr(&cb->mb_t[t2.slot]), (uint32_t)lane));
     }
   }
 }
@@ -487,10 +557,17 @@ struct IntC {
 // On exit rnorm is the normaliser inv(sum Y) (1 when PAM_F_NO_NORMALIZE).
 // v holds Y^(T+1) unless final_xch reused the registers.  Returns the row
 // status, identical in every CTA.
-template <typename Elem, int NTG, int E, int P, bool ARGMAX, typename Hooks>
+//
+// STOP (early stopping): after every non-final pass the exchange
+// also carries the row maximum; when max Y / sum Y >= 1 - eps_stop (the
+// oracle's test, oracle.c orc_cutmax) the remaining iterations are replaced by
+// one terminal pass Y = v + K (undo the storage shift) that feeds the usual
+// final exchange, normaliser and argmax.  The decision is made by every CTA's
+// control warp from identical exchanged sums, so it is cluster-uniform.
+template <typename Elem, int NTG, int E, int P, bool ARGMAX, typename Hooks, bool STOP = false>
 __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, const double Q_in, const double K0,
                                               const int len, const double mph, const RowParams& rp,
-                                              const double inv_n,
+                                              const double inv_n, const double nd,
                                               ControlBlock* cb, uint32_t& xround, const uint32_t rank,
                                               const uint32_t C, const int gtid, const int64_t gbase,
                                               double* stats_row, double& rnorm, long long& argmax_out, Hooks& h,
@@ -539,15 +616,18 @@ __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, c
   double kcur = K0;
   Elem w = 0;  // phantom value (shifted representation)
 
-  // one element pass; FIRST: fused pass-0 side work, LAST: argmax, no moments
-  auto pass = [&](auto first_c, auto last_c, Elem ke, Elem be, Elem kn, int p, Elem& sa, Elem& sb, Elem& qa,
-                  Elem& qb, Elem& bestv, int& besto) {
+  // one element pass; FIRST: fused pass-0 side work, LAST: argmax, no moments;
+  // TERM (early stop): y = v + ke, the stored shift undone, instead of an update
+  auto pass = [&](auto first_c, auto last_c, auto term_c, Elem ke, Elem be, Elem kn, int p, Elem& sa, Elem& sb,
+                  Elem& qa, Elem& qb, Elem& bestv, int& besto) {
     constexpr bool FIRST = decltype(first_c)::value, LAST = decltype(last_c)::value;
+    constexpr bool TERM = decltype(term_c)::value;
+    constexpr bool TRACK = (LAST && ARGMAX) || (STOP && !LAST);  // STOP: the row max of every iterate
 #pragma unroll
     for (int i = 0; i < E; i += 2) {
       if (FIRST && (i % VEC) == 0) h.pass0(i / VEC);
-      const Elem d0 = cutmax_update<Elem, P>(v[i], ke, be, kn, p);
-      const Elem d1 = cutmax_update<Elem, P>(v[i + 1], ke, be, kn, p);
+      const Elem d0 = TERM ? v[i] + ke : cutmax_update<Elem, P>(v[i], ke, be, kn, p);
+      const Elem d1 = TERM ? v[i + 1] + ke : cutmax_update<Elem, P>(v[i + 1], ke, be, kn, p);
       v[i] = d0;
       v[i + 1] = d1;
       if (real(i)) {
@@ -558,12 +638,15 @@ __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, c
         sb += d1;
         if (!LAST) qb = fma_e(d1, d1, qb);
       }
-      if (LAST && ARGMAX) {  // slots in increasing element order: strict > keeps the lowest index
+      if (TRACK) {  // slots in increasing element order: strict > keeps the lowest index
         if (d0 > bestv) { bestv = d0; besto = i; }
         if (d1 > bestv) { bestv = d1; besto = i + 1; }
       }
     }
     if (FIRST) ptx::fence_proxy_async_smem();  // side writes -> visible to the TMA engine after the barrier
+  };
+  auto slot_index = [&](int besto) {
+    return gbase + (long long)(((besto / VEC) * NTG + gtid) * VEC + (besto % VEC));
   };
 
   // scalar chain of iteration t from (kcur, dm, s2): status, 1/sigma, k, b
@@ -613,35 +696,41 @@ __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, c
   // ---- T iterations; the last one (no variance; argmax) is peeled -----------
   double total = 0.0;
   double kd, bd;
+  bool stopped = false;  // STOP: eps_stop reached, the next pass is the terminal one
   chain(0, kd, bd);  // every warp: identical inputs
   for (int t = 0; t < T; ++t) {
     const Elem ke = (Elem)kd, be = affine_coef<Elem>(bd, dm), kn = (Elem)(-knext);
     const int p = pcur;
-    w = cutmax_update<Elem, P>(w, ke, be, kn, p);
+    if (!stopped) w = cutmax_update<Elem, P>(w, ke, be, kn, p);
     const double kthis = knext;
     const bool first = (t == 0) && h.pass0_on;
     Elem sa = 0, sb = 0, qa = 0, qb = 0, bestv = -INFINITY;
     int besto = 0;  // register slot of the best element (compile-time immediates)
-    if (t + 1 < T) {
+    if (t + 1 < T && !stopped) {
       if (first)
-        pass(BoolC<true>(), BoolC<false>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
+        pass(BoolC<true>(), BoolC<false>(), BoolC<false>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
       else
-        pass(BoolC<false>(), BoolC<false>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
+        pass(BoolC<false>(), BoolC<false>(), BoolC<false>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
       c_inv = rp.inv_c[t + 1];  // prefetch next iteration's constants
       knext = rp.kshift[t + 2];
       pcur = rp.p[t + 1];
       PAM_TRACE(tr, 5 + 2 * t);
-      xch_push<NTG, kSum2>((double)sa + (double)sb, (double)qa + (double)qb, 0.0, 0LL, cb, xround, rank, C, gtid,
-                           [&]() { h.side(t); });
+      constexpr int XM = STOP ? kArgmax : kSum2;
+      xch_push<NTG, XM>((double)sa + (double)sb, (double)qa + (double)qb, (double)bestv, slot_index(besto), cb,
+                        xround, rank, C, gtid, [&]() { h.side(t); });
       kcur = kthis;
       const double wd = (double)w;
       if (warp == 0) {
         double bv = 0.0;
         long long bi = 0;
-        const double2 r = xch_wait<kSum2>(bv, bi, cb, xround, C, gtid);
+        const double2 r = xch_wait<XM>(bv, bi, cb, xround, C, gtid);
         const double Q = r.y - mph * wd * wd;
         moments_from_sums(r.x - mph * wd, Q, inv_n, dm, s2);
-        if (st == PAM_OK && isfinite(Q) && Q * inv_n > kGuard * s2) {
+        // stop when the top mass max Y / sum Y reaches 1 - eps_stop
+        const bool stop_here = STOP && st == PAM_OK && (bv + kcur) / fma(nd, kcur, r.x - mph * wd) >= 1.0 - rp.eps_stop;
+        if (stop_here) {
+          publish(0.0, 0.0, 2);
+        } else if (st == PAM_OK && isfinite(Q) && Q * inv_n > kGuard * s2) {
           publish(0.0, 0.0, 1);  // exact second pass first
         } else {
           chain(t + 1, kd, bd);
@@ -652,6 +741,12 @@ __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, c
       }
       bar1();
       Bcast b = cb->bc;
+      if (STOP && b.flag == 2) {  // cluster-uniform: the next iteration is the terminal pass
+        stopped = true;
+        st = b.st;
+        PAM_TRACE(tr, 6 + 2 * t);
+        continue;
+      }
       if (b.flag) {  // exact second pass about dm (cluster-uniform, rare)
         dm = b.dm;
         const Elem dme = (Elem)dm;
@@ -678,17 +773,23 @@ __device__ __forceinline__ int cutmax_iterate(Elem (&v)[E], const double S_in, c
       st = b.st;
       PAM_TRACE(tr, 6 + 2 * t);
     } else {
-      if (first)
-        pass(BoolC<true>(), BoolC<true>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
-      else
-        pass(BoolC<false>(), BoolC<true>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
+      if (STOP && stopped) {
+        const Elem kk = (Elem)kcur;  // Y = v + K: the shift of the stored iterate undone
+        w = w + kk;
+        pass(BoolC<false>(), BoolC<true>(), BoolC<true>(), kk, be, kn, p, sa, sb, qa, qb, bestv, besto);
+      } else if (first) {
+        pass(BoolC<true>(), BoolC<true>(), BoolC<false>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
+      } else {
+        pass(BoolC<false>(), BoolC<true>(), BoolC<false>(), ke, be, kn, p, sa, sb, qa, qb, bestv, besto);
+      }
       double best = (double)bestv;
-      long long besti = gbase + (long long)(((besto / VEC) * NTG + gtid) * VEC + (besto % VEC));
+      long long besti = slot_index(besto);
       PAM_TRACE(tr, 5 + 2 * t);
       const double ty = h.final_xch((double)sa + (double)sb, best, besti);
       PAM_TRACE(tr, 6 + 2 * t);
-      total = ty - mph * (double)w;  // kshift[T] == 0: v holds Y^(T+1) itself
+      total = ty - mph * (double)w;  // kshift[T] == 0 (or the terminal pass): v holds Y itself
       argmax_out = besti;
+      break;
     }
   }
 
@@ -718,9 +819,10 @@ constexpr int min_blocks_for() {
 }
 
 // ---------------------------------------------------------------------------
-template <typename Elem, int NTG, int E, int P, int MINB = 0>
+template <typename Elem, int NTG, int E, int P, int MINB = 0, bool STOP = false>
 __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, NTG, E>()))
     cutmax_rows_kernel(const CutmaxArgs a) {
+  static_assert(!STOP || P == 0, "early stopping runs on the generic flow");
   using Tr = ElemTraits<Elem>;
   using V = typename Tr::V;
   constexpr int VEC = Tr::VEC;
@@ -767,6 +869,8 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[0]), 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[1]), 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_in), 1);
+    ptx::mbar_init(ptx::smem_addr(&cb->mb_t[0]), 1);
+    ptx::mbar_init(ptx::smem_addr(&cb->mb_t[1]), 1);
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -774,6 +878,8 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 32u);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 32u);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_in), C * 16u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[0]), C * 16u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[1]), C * 16u);
   }
   ptx::cluster_sync();
 
@@ -785,7 +891,6 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
     ptx::bulk_g2s(ptx::smem_addr(buf) + off, src + off, nb, bar_load, policy);
   };
   auto store_all = [&](int64_t row) {  // buf -> Z(row), one bulk group per chunk
-    if (a.debug_flags & 1) return;
     unsigned char* dst = reinterpret_cast<unsigned char*>(Z + row * a.ldz + base);
     for (int i = 0; i < nch; ++i) {
       const uint32_t off = (uint32_t)i * chunk;
@@ -796,16 +901,33 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
   };
   auto load_after_store = [&](int64_t row) {  // X(row) -> buf as the outstanding store frees each chunk
     ptx::mbar_arrive_expect_tx(bar_load, slice_bytes);
-    const bool st_out = !(a.debug_flags & 1);
     for (int i = 0; i < nch; ++i) {
-      if (st_out) ptx::bulk_wait_read_le(nch - 1 - i);
+      ptx::bulk_wait_read_le(nch - 1 - i);
       load_chunk(row, i);
     }
   };
 
   int64_t row = cid;
   uint32_t xround = 0, load_par = 0, in_par = 0;
+  uint32_t t2_ph = 0u;           // mb_t phases, bit s = slot s (warp 0)
+  int64_t lrow = 0;              // local row counter: the parity selects the top-2 record slot
   Elem v[E];
+  // top-2 of the real input elements of this thread's slots (TieWarning);
+  // phantom slots are copies of x[0] and must not count as a second maximum
+  Elem t1 = -INFINITY, t2 = -INFINITY;
+  auto load_direct = [&](const Elem* src, Elem k0e) {  // unaligned rows: direct loads, no staging
+#pragma unroll
+    for (int kk = 0; kk < NV; ++kk) {
+      const int li0 = (kk * NTG + gtid) * VEC;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        const bool in = li0 + j < len;
+        const Elem xv = in ? __ldcs(src + li0 + j) : k0e;
+        v[kk * VEC + j] = xv;
+        if (in) top2_add(t1, t2, xv);
+      }
+    }
+  };
 
   // ---- prologue: the cluster's first row -> registers -------------------------
   if (TMA && row < a.B) {
@@ -821,9 +943,15 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       const int li0 = (k * NTG + gtid) * VEC;
       if (li0 + VEC <= len) {
         *reinterpret_cast<V*>(&v[k * VEC]) = *reinterpret_cast<const V*>(buf + li0);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) top2_add(t1, t2, v[k * VEC + j]);
       } else {
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) v[k * VEC + j] = (li0 + j < len) ? buf[li0 + j] : k0;  // phantoms = K0
+        for (int j = 0; j < VEC; ++j) {
+          const bool in = li0 + j < len;
+          v[k * VEC + j] = in ? buf[li0 + j] : k0;  // phantoms = K0
+          if (in) top2_add(t1, t2, v[k * VEC + j]);
+        }
       }
     }
     __syncthreads();  // buf free
@@ -857,10 +985,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
     double S_c = 0.0, Q_c = 0.0, R_c = 0.0;  // warp 0: cluster sums of the current iterate
     Elem k0_cur = row < a.B ? __ldg(X + row * a.ldx) : Elem(0);
     auto bar1 = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(NTG) : "memory"); };
-#ifdef PAM_TRACE_BUILD
-    int64_t lrow = 0;
-#endif
-    for (; row < a.B; row += ncl) {
+    for (; row < a.B; row += ncl, ++lrow) {
       const int64_t next = row + ncl;
       const bool has_next = next < a.B;
       const bool merged = TMA && has_next;  // the closing exchange carries the next row's input sums
@@ -878,17 +1003,13 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       // x[next][0]: loaded a row ahead, first used by the last pass
       const Elem k0next = has_next ? __ldg(X + next * a.ldx) : Elem(0);
       if (!in_ready) {
-        if (!TMA) {  // unaligned rows: direct loads, no staging
-          const Elem* src = xrow + base;
-#pragma unroll
-          for (int kk = 0; kk < NV; ++kk) {
-            const int li0 = (kk * NTG + gtid) * VEC;
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) v[kk * VEC + j] = (li0 + j < len) ? __ldcs(src + li0 + j) : k0e;
-          }
+        if (!TMA) {
+          t1 = t2 = -INFINITY;
+          load_direct(xrow + base, k0e);
         }
         const double3 part = input_pass3<Elem, E>(v, K0);
-        const double3 r = cluster_sum3<NTG>(part.x, part.y, part.z, cb, xround, rank, C, gtid);
+        const double3 r = cluster_sum3<NTG>(part.x, part.y, part.z, cb, xround, rank, C, gtid,
+                                            Top2Push{true, (double)t1, (double)t2, (uint32_t)(lrow & 1)});
         S_c = r.x;
         Q_c = r.y;
         R_c = r.z;
@@ -904,9 +1025,8 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
           ptx::mbar_arrive_expect_tx(bar_load, slice_bytes);
           armed = true;
         }
-        const bool st_out = !(a.debug_flags & 1);
         for (; issued < upto; ++issued) {
-          if (st_out) ptx::bulk_wait_read_le(nch - 1 - issued);
+          ptx::bulk_wait_read_le(nch - 1 - issued);
           load_chunk(next, issued);
         }
       };
@@ -1182,6 +1302,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       int besto = 0;  // register slot of the best element (compile-time immediates)
       double3 nxt = make_double3(0.0, 0.0, 0.0);
       Elem* zrow = Z + row * a.ldz + base;
+      t1 = t2 = -INFINITY;  // top-2 of X(next) (merged)
       auto last = [&](auto mode_c, auto r_c) {
         constexpr int MODE = decltype(mode_c)::value;  // 0: swap (merged), 1: Z -> buffer, 2: Z -> HBM
         constexpr bool R3 = decltype(r_c)::value;
@@ -1200,11 +1321,9 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
             o[j] = y * re;
           }
           if (MODE == 2) {
-            if (!(a.debug_flags & 1)) {
 #pragma unroll
-              for (int j = 0; j < VEC; ++j)
-                if (li0 + j < len) __stcs(zrow + li0 + j, o[j]);
-            }
+            for (int j = 0; j < VEC; ++j)
+              if (li0 + j < len) __stcs(zrow + li0 + j, o[j]);
             continue;
           }
           if (li0 + VEC <= len) {
@@ -1214,14 +1333,20 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
             if (MODE == 0) {
               const Elem* xe = reinterpret_cast<const Elem*>(&xn);
 #pragma unroll
-              for (int j = 0; j < VEC; ++j) v[kk * VEC + j] = xe[j] - k0next;
+              for (int j = 0; j < VEC; ++j) {
+                v[kk * VEC + j] = xe[j] - k0next;
+                top2_add(t1, t2, xe[j]);
+              }
             }
           } else {
 #pragma unroll
             for (int j = 0; j < VEC; ++j) {
               const bool in = li0 + j < len;
               Elem xv = k0next;  // phantoms: K0(next) -> 0
-              if (MODE == 0 && in) xv = buf[li0 + j];
+              if (MODE == 0 && in) {
+                xv = buf[li0 + j];
+                top2_add(t1, t2, xv);
+              }
               if (in) buf[li0 + j] = o[j];
               if (MODE == 0) v[kk * VEC + j] = xv - k0next;
             }
@@ -1262,9 +1387,9 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       double best = (double)bestv;
       long long besti = base + (long long)(((besto / VEC) * NTG + gtid) * VEC + (besto % VEC));
       const int64_t zr = row;
-      xch_push<NTG, kArgmax>(nxt.x, nxt.y, best, besti, cb, xround, rank, C, gtid, [&]() {
-        if (TMA) store_all(zr);
-      });
+      xch_push<NTG, kArgmax>(
+          nxt.x, nxt.y, best, besti, cb, xround, rank, C, gtid, [&]() { if (TMA) store_all(zr); }, true,
+          Top2Push{merged, (double)t1, (double)t2, (uint32_t)((lrow + 1) & 1)});
       if (merged && T == 1) {
         // T = 1 needs the next input's third power sum too (one more exchange)
         if (warp == 0) {
@@ -1286,14 +1411,14 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       PAM_TRACE(tr, 6 + 2 * (T - 1));
       in_ready = merged;
       k0_cur = k0next;
-      if (rank == 0 && gtid == 0) {
-        if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)besti : -1;
-        if (a.status) a.status[row] = st;
+      if (warp == 0) {  // this row's input top-2 arrived long ago (input / previous closing exchange)
+        const double2 tt = top2_wait(cb, (uint32_t)(lrow & 1), t2_ph, C, gtid);
+        if (rank == 0 && gtid == 0) {
+          if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)besti : -1;
+          if (a.status) a.status[row] = st | tie_flag(st, tt);
+        }
       }
       PAM_TRACE(tr, 21);
-#ifdef PAM_TRACE_BUILD
-      ++lrow;
-#endif
     }
   } else {
     // ===== generic p: one-pass-late normalisation (see header) ==============
@@ -1304,10 +1429,8 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
     Elem rn_prev = 1;
     int64_t zrow_prev = 0;
     const int pf_ex = T >= 3 ? 1 : 0;  // exchange whose DMA hook issues the next row's load
-  #ifdef PAM_TRACE_BUILD
-    int64_t lrow = 0;
-  #endif
-    for (; row < a.B; row += ncl) {
+    const int warp = gtid >> 5;
+    for (; row < a.B; row += ncl, ++lrow) {
       const int64_t next = row + ncl;
       const bool has_next = next < a.B;
       const bool merged = TMA && has_next;  // row-boundary exchange carries the next row's input sums
@@ -1325,17 +1448,13 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       const Elem k0next = has_next ? __ldg(X + next * a.ldx) : Elem(0);
 
       if (!in_ready) {
-        if (!TMA) {  // unaligned rows: direct loads, no staging
-          const Elem* src = xrow + base;
-  #pragma unroll
-          for (int kk = 0; kk < NV; ++kk) {
-            const int li0 = (kk * NTG + gtid) * VEC;
-  #pragma unroll
-            for (int j = 0; j < VEC; ++j) v[kk * VEC + j] = (li0 + j < len) ? __ldcs(src + li0 + j) : k0e;
-          }
+        if (!TMA) {
+          t1 = t2 = -INFINITY;
+          load_direct(xrow + base, k0e);
         }
         const double2 part = input_pass<Elem, E>(v, K0);
-        const double2 r = cluster_sum2<NTG>(part.x, part.y, cb, xround, rank, C, gtid);
+        const double2 r = cluster_sum2<NTG>(part.x, part.y, cb, xround, rank, C, gtid,
+                                            Top2Push{true, (double)t1, (double)t2, (uint32_t)(lrow & 1)});
         S_in = r.x;
         Q_in = r.y;
       }
@@ -1371,8 +1490,9 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
           ptx::mbar_wait_cta(bar_load, load_par);  // X(next) has landed
           load_par ^= 1u;
           PAM_TRACE(tr, 23);
-          // swap: Y -> buf, X(next) - K0(next) -> registers (+ its moments)
+          // swap: Y -> buf, X(next) - K0(next) -> registers (+ its moments and top-2)
           Elem sa = 0, sb = 0, qa = 0, qb = 0;
+          t1 = t2 = -INFINITY;
   #pragma unroll
           for (int kk = 0; kk < NV; ++kk) {
             const int li0 = (kk * NTG + gtid) * VEC;
@@ -1381,13 +1501,19 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
               *reinterpret_cast<V*>(buf + li0) = *reinterpret_cast<const V*>(&v[kk * VEC]);
               const Elem* xe = reinterpret_cast<const Elem*>(&xn);
   #pragma unroll
-              for (int j = 0; j < VEC; ++j) v[kk * VEC + j] = xe[j] - k0next;
+              for (int j = 0; j < VEC; ++j) {
+                v[kk * VEC + j] = xe[j] - k0next;
+                top2_add(t1, t2, xe[j]);
+              }
             } else {
   #pragma unroll
               for (int j = 0; j < VEC; ++j) {
                 const bool in = li0 + j < len;
                 const Elem xv = in ? buf[li0 + j] : k0next;  // phantoms: K0(next) -> 0
-                if (in) buf[li0 + j] = v[kk * VEC + j];
+                if (in) {
+                  buf[li0 + j] = v[kk * VEC + j];
+                  top2_add(t1, t2, xv);
+                }
                 v[kk * VEC + j] = xv - k0next;
               }
             }
@@ -1400,7 +1526,8 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
               qb = fma_e(d1, d1, qb);
             }
           }
-          xin_push<NTG>((double)sa + (double)sb, (double)qa + (double)qb, cb, rank, C, gtid);
+          xin_push<NTG>((double)sa + (double)sb, (double)qa + (double)qb, cb, rank, C, gtid,
+                        Top2Push{true, (double)t1, (double)t2, (uint32_t)((lrow + 1) & 1)});
           PAM_TRACE(tr, 24);
         }
         double2 r = xch_wait<kArgmax>(best, besti, cb, xround, C, gtid);
@@ -1415,13 +1542,16 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
 
       double rnorm = 1.0;
       long long amax = -1;
-      const int st = cutmax_iterate<Elem, NTG, E, P, true>(
-          v, S_in, Q_in, K0, len, mph, rp, a.inv_n, cb, xround, rank, C, gtid, base,
+      const int st = cutmax_iterate<Elem, NTG, E, P, true, decltype(hooks), STOP>(
+          v, S_in, Q_in, K0, len, mph, rp, a.inv_n, (double)n, cb, xround, rank, C, gtid, base,
           (rank == 0 && gtid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr, rnorm, amax, hooks, tr);
       PAM_TRACE(tr, 20);
-      if (rank == 0 && gtid == 0) {
-        if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)amax : -1;
-        if (a.status) a.status[row] = st;
+      if (warp == 0) {
+        const double2 tt = top2_wait(cb, (uint32_t)(lrow & 1), t2_ph, C, gtid);
+        if (rank == 0 && gtid == 0) {
+          if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)amax : -1;
+          if (a.status) a.status[row] = st | tie_flag(st, tt);
+        }
       }
 
       const Elem re = (Elem)rnorm;
@@ -1454,7 +1584,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
           ptx::fence_proxy_async_smem();  // make the Z writes visible to the TMA engine
           __syncthreads();
           if (dma) store_all(row);
-        } else if (!(a.debug_flags & 1)) {
+        } else {
           Elem* zrow = Z + row * a.ldz + base;
   #pragma unroll
           for (int kk = 0; kk < NV; ++kk) {
@@ -1467,9 +1597,6 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       }
       k0_cur = k0next;
       PAM_TRACE(tr, 21);
-  #ifdef PAM_TRACE_BUILD
-      ++lrow;
-  #endif
     }
   }
   if (TMA && dma) ptx::bulk_wait_all();  // Z stores complete before the CTA retires

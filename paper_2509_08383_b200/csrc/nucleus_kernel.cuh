@@ -38,8 +38,9 @@ struct SamplerArgs {
   RowParams rp;
 };
 
-template <int NT, int E, int P, bool GUMBEL>
+template <int NT, int E, int P, bool GUMBEL, bool STOP = false>
 __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a) {
+  static_assert(!STOP || P == 0, "early stopping runs on the generic flow");
   constexpr int VEC = 2;
   constexpr int NV = E / VEC;
   constexpr int NW = NT / 32;
@@ -68,6 +69,8 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[0]), 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[1]), 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_g), 1);
+    ptx::mbar_init(ptx::smem_addr(&cb->mb_t[0]), 1);
+    ptx::mbar_init(ptx::smem_addr(&cb->mb_t[1]), 1);
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -75,10 +78,12 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 32u);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 32u);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_g), C * 32u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[0]), C * 16u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[1]), C * 16u);
   }
   ptx::cluster_sync();
 
-  uint32_t xround = 0, load_par = 0, g_par = 0;
+  uint32_t xround = 0, load_par = 0, g_par = 0, t2_ph = 0;
   double v[E];
 
   int64_t lrow = 0;
@@ -147,6 +152,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
       __syncthreads();
     }
     double xmax = -HUGE_VAL;
+    double t1 = -HUGE_VAL, t2 = -HUGE_VAL;  // top-2 of x~ (TieWarning on the vector CutMax sees)
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const int li0 = (k * NT + tid) * VEC;
@@ -155,6 +161,8 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
         v[k * VEC + 0] = t.x + v[k * VEC + 0];  // Alg. 3 line 5: x~ = x + G
         v[k * VEC + 1] = t.y + v[k * VEC + 1];
         xmax = fmax(xmax, fmax(t.x, t.y));
+        top2_add(t1, t2, v[k * VEC + 0]);
+        top2_add(t1, t2, v[k * VEC + 1]);
       } else {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
@@ -162,6 +170,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
             const double xv = buf[li0 + j];
             v[k * VEC + j] = xv + v[k * VEC + j];
             xmax = fmax(xmax, xv);
+            top2_add(t1, t2, v[k * VEC + j]);
           } else {
             v[k * VEC + j] = K0;  // phantom (see cutmax_iterate)
           }
@@ -173,16 +182,20 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     double rnorm = 1.0;
     long long unused_argmax;
     const double2 part = input_pass<double, E>(v, K0);
-    const double2 rin = cluster_sum2<NT>(part.x, part.y, cb, xround, rank, C, tid);
+    const double2 rin = cluster_sum2<NT>(part.x, part.y, cb, xround, rank, C, tid,
+                                         Top2Push{true, t1, t2, (uint32_t)(lrow & 1)});
     auto final_xch = [&](double sy, double& bv, long long& bi) -> double {
       return cluster_reduce<NT, false>(sy, 0.0, bv, bi, cb, xround, rank, C, tid).x;
     };
     auto hooks = make_hooks(false, [](int) {}, [](int) {}, final_xch);
-    int st = cutmax_iterate<double, NT, E, P, false>(v, rin.x, rin.y, K0, len, (double)((int64_t)C * NT * E - n), a.rp, a.inv_n, cb, xround, rank, C,
-                                                     tid, base, nullptr, rnorm, unused_argmax, hooks, nullptr);
+    int st = cutmax_iterate<double, NT, E, P, false, decltype(hooks), STOP>(
+        v, rin.x, rin.y, K0, len, (double)((int64_t)C * NT * E - n), a.rp, a.inv_n, (double)n, cb, xround, rank, C,
+        tid, base, nullptr, rnorm, unused_argmax, hooks, nullptr);
 
     PAM_TRACE(tr, 3);
-    // token candidate over Z = Y * rnorm (and optional one-hot store)
+    // token = argmax of Y^(T+1) before the normalisation (pin A7, oracle.c
+    // orc_cutmax: Y * inv(sum Y) could round a near-tie into an exact one);
+    // the optional one-hot output is Z = Y * rnorm
     double best = -HUGE_VAL, bestx = 0.0;
     long long besti = 0x7fffffffffffffffLL;
 #pragma unroll
@@ -190,10 +203,11 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
       const int li0 = (k * NT + tid) * VEC;
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
-        const double o = v[k * VEC + j] * rnorm;
+        const double y = v[k * VEC + j];
+        const double o = y * rnorm;
         if (li0 + j < len) {
-          if (o > best) {
-            best = o;
+          if (y > best) {
+            best = y;
             besti = base + li0 + j;
             bestx = buf[li0 + j];
           }
@@ -284,10 +298,13 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     }
     const double2 ta = cluster_sum2<NT>(tot, above, cb, xround, rank, C, tid);
     PAM_TRACE(tr, 5);
-    if (rank == 0 && tid == 0) {
-      if (a.token) a.token[row] = (st == PAM_OK) ? (int32_t)besti : -1;
-      if (a.inside) a.inside[row] = (st == PAM_OK && ta.y < a.p_nucleus * ta.x) ? 1 : 0;
-      if (a.status) a.status[row] = st;
+    if (warp == 0) {
+      const double2 tt = top2_wait(cb, (uint32_t)(lrow & 1), t2_ph, C, tid);
+      if (rank == 0 && tid == 0) {
+        if (a.token) a.token[row] = (st == PAM_OK) ? (int32_t)besti : -1;
+        if (a.inside) a.inside[row] = (st == PAM_OK && ta.y < a.p_nucleus * ta.x) ? 1 : 0;
+        if (a.status) a.status[row] = st | tie_flag(st, tt);
+      }
     }
   }
   ptx::cluster_sync();

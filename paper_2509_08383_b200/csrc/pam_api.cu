@@ -10,11 +10,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/pam_c_api.h"
 #include "analysis_kernel.cuh"
-#include "cutmax_ahead_kernel.cuh"
 #include "cutmax_kernel.cuh"
 #include "nucleus_kernel.cuh"
 #include "pam_variants.h"
@@ -34,7 +34,26 @@ int cuda_fail(cudaError_t e, const char* what) {
   return PAM_ERR_CUDA;
 }
 
-// Kernel tables: pam_variants.h (defined in cutmax_variants.cu / sampler_variants.cu).
+// Tuning/test overrides (pam_set_geometry_override, pam_set_host_chunk_bytes).
+// Explicit API calls only: the library reads no environment variables.
+struct Overrides {
+  std::atomic<int> ntg[2]{{0}, {0}}, e[2]{{0}, {0}}, c[2]{{0}, {0}}, minb[2]{{0}, {0}};  // [fp32, fp64]
+  std::atomic<int64_t> host_chunk_bytes{128ll << 20};
+  std::atomic<int> generation{0};  // bumped on every override change: invalidates the geometry cache
+};
+Overrides g_ovr;
+
+// Kernel tables: pam_variants.h (cutmax_variants_f64.cu / _f32.cu, sampler_variants.cu).
+const VariantTable kCutmaxTables[2] = {{kCutmaxVariantsF32, kNumCutmaxVariantsF32},
+                                       {kCutmaxVariantsF64, kNumCutmaxVariantsF64}};
+
+// Kernel flavour of a CutMax launch: 0 generic p, 1 p = 3 everywhere, 2 generic with early stop.
+int flavour_of(const pam_cutmax_params* prm) {
+  if (prm->eps_stop > 0.0) return 2;
+  for (int t = 0; t < prm->T; ++t)
+    if (prm->p[t] != 3) return 0;
+  return 1;
+}
 
 struct Geometry {
   const Variant* var = nullptr;
@@ -42,88 +61,39 @@ struct Geometry {
   int L = 0;
 };
 
-// Dev override: PAM_FORCE_CFG_F64 / PAM_FORCE_CFG_F32 = "NTG,E,C[,MINB]".
-bool parse_force(int elem_bytes, int* ntg, int* e, int* c, int* minb) {
-  const char* s = getenv(elem_bytes == 8 ? "PAM_FORCE_CFG_F64" : "PAM_FORCE_CFG_F32");
-  if (!s || !*s) return false;
-  *minb = 0;
-  return sscanf(s, "%d,%d,%d,%d", ntg, e, c, minb) >= 3;
-}
-
 int buffer_bytes(const Variant& v) { return ((v.ntg * v.e * v.elem_bytes + 127) / 128) * 128; }
 int smem_bytes(const Variant& v) { return buffer_bytes(v) + (int)sizeof(ControlBlock); }
 
 int64_t slice_len(int64_t n, int C, int vec) { return ((n + C - 1) / C + vec - 1) / vec * vec; }
 
-int max_active_clusters(const void* fn, int nt, int C, int smem);
-
-// Launch geometry.  Candidates are every (variant, cluster size C = 1..16)
-// whose per-CTA capacity covers the slice ceil(n/C) with < 30% phantom waste.
-// They are ranked by rows per microsecond, clusters / t_row, with the row
-// period fitted to B200 measurements (tools/tune.py, tools/trace.py):
-//   t_row ~= a + b * cap * k
-// a = latency per row (T exchanges + scalar chains: fp64 4.8 us, fp32 2.5 us),
-// b = element cost per CTA-slot (fp64 0.33 ns, fp32 0.35 ns), cap = NTG*E, and
-// k = CTAs sharing an SM (clusters*C / #SMs, rounded up) from the occupancy
-// query.  Non power-of-two clusters matter: 9-CTA clusters pack 135 SMs vs 120
-// for 8.
-Geometry choose_geometry(int elem_bytes, int64_t B, int64_t n) {
-  Geometry g;
-  const int vec = 16 / elem_bytes;
-  int fntg, fe, fc, fmb;
-  if (parse_force(elem_bytes, &fntg, &fe, &fc, &fmb)) {
-    for (int i = 0; i < kNumCutmaxVariants; ++i) {
-      const Variant& v = kCutmaxVariants[i];
-      if (v.elem_bytes == elem_bytes && v.ntg == fntg && v.e == fe && v.minb == fmb) {
-        const int64_t L = slice_len(n, fc, vec);
-        if ((int64_t)v.ntg * v.e >= L) { g.var = &v; g.C = fc; g.L = (int)L; return g; }
-      }
-    }
-  }
-  int dev = 0;
-  const bool have_gpu = cudaGetDevice(&dev) == cudaSuccess;
-  int nsm = 148;
-  if (have_gpu && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
-  const double a_us = elem_bytes == 8 ? 4.8 : 2.5, b_ns = elem_bytes == 8 ? 0.33 : 0.35;
-  double best_score = -1.0;
-  for (int C = 1; C <= 16; ++C) {
-    const int64_t L = slice_len(n, C, vec);
-    for (int i = 0; i < kNumCutmaxVariants; ++i) {
-      const Variant& v = kCutmaxVariants[i];
-      if (v.elem_bytes != elem_bytes) continue;
-      const int64_t cap = (int64_t)v.ntg * v.e;
-      if (cap < L || (C > 1 && cap > L + L * 3 / 10)) continue;
-      if (C > 1 && L < 2048) continue;  // tiny slices: exchanges would dominate
-      const int smem = smem_bytes(v);
-      if (smem > 227 * 1024) continue;
-      const int active = have_gpu ? max_active_clusters(v.fn[1], v.ntg, C, smem) : nsm / C;
-      if (active <= 0) continue;
-      const int64_t clusters = (B < active) ? B : active;
-      const int64_t k = (clusters * C + nsm - 1) / nsm;
-      const double t_us = a_us + 1e-3 * b_ns * (double)cap * (double)(k < 1 ? 1 : k);
-      const double score = (double)clusters / t_us - 1e-9 * (double)C;  // tie-break: smaller clusters
-      if (score > best_score) { best_score = score; g.var = &v; g.C = C; g.L = (int)L; }
-    }
-  }
-  cudaGetLastError();
-  return g;
-}
-
-struct OccKey {
+// ---- per-device kernel attributes and occupancy -------------------------------
+// cudaFuncSetAttribute applies per device context, so both caches are keyed by
+// the device ordinal as well as the kernel.
+std::mutex g_occ_mu;
+struct FnKey {
+  int dev;
   const void* fn;
   int C, smem;
+  bool operator==(const FnKey& o) const { return dev == o.dev && fn == o.fn && C == o.C && smem == o.smem; }
 };
-std::mutex g_occ_mu;
-std::vector<std::pair<OccKey, int>> g_occ_cache;
+std::vector<std::pair<FnKey, int>> g_occ_cache;      // (dev, fn, C, smem) -> max active clusters
+std::vector<std::pair<FnKey, int>> g_smem_attr;      // (dev, fn) -> largest dynamic smem opted in
 
-std::vector<std::pair<const void*, int>> g_smem_attr;  // per kernel: largest dynamic smem opted in
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return dev;
+}
 
-// Raise the kernel's dynamic-smem opt-in to at least `smem` (never lower it:
-// an earlier, larger cached configuration must stay launchable).
-void ensure_smem_attr(const void* fn, int smem, int C) {
+// Raise the kernel's dynamic-smem opt-in on this device to at least `smem`
+// (never lower it: an earlier, larger configuration must stay launchable).
+void ensure_smem_attr(int dev, const void* fn, int smem) {
   std::lock_guard<std::mutex> lk(g_occ_mu);
   for (auto& kv : g_smem_attr)
-    if (kv.first == fn) {
+    if (kv.first.dev == dev && kv.first.fn == fn) {
       if (kv.second >= smem) return;
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       kv.second = smem;
@@ -131,16 +101,17 @@ void ensure_smem_attr(const void* fn, int smem, int C) {
     }
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  g_smem_attr.push_back({fn, smem});
-  (void)C;
+  g_smem_attr.push_back({FnKey{dev, fn, 0, 0}, smem});
 }
 
 int max_active_clusters(const void* fn, int nt, int C, int smem) {
-  ensure_smem_attr(fn, smem, C);
+  const int dev = current_device();
+  ensure_smem_attr(dev, fn, smem);
+  const FnKey key{dev, fn, C, smem};
   {
     std::lock_guard<std::mutex> lk(g_occ_mu);
     for (auto& kv : g_occ_cache)
-      if (kv.first.fn == fn && kv.first.C == C && kv.first.smem == smem) return kv.second;
+      if (kv.first == key) return kv.second;
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -159,8 +130,97 @@ int max_active_clusters(const void* fn, int nt, int C, int smem) {
     ncl = 0;
   }
   std::lock_guard<std::mutex> lk(g_occ_mu);
-  g_occ_cache.push_back({OccKey{fn, C, smem}, ncl});
+  g_occ_cache.push_back({key, ncl});
   return ncl;
+}
+
+// Launch geometry.  Candidates are every (variant, cluster size C = 1..16)
+// whose per-CTA capacity covers the slice ceil(n/C) with < 30% phantom waste.
+// They are ranked by rows per microsecond, clusters / t_row, with the row
+// period fitted to B200 measurements (tools/tune.py, tools/trace.py):
+//   t_row ~= a + b * cap * k
+// a = latency per row (T exchanges + scalar chains: fp64 4.8 us, fp32 2.5 us),
+// b = element cost per CTA-slot (fp64 0.33 ns, fp32 0.35 ns), cap = NTG*E, and
+// k = CTAs sharing an SM (clusters*C / #SMs, rounded up) from the occupancy
+// query.  Non power-of-two clusters matter: 9-CTA clusters pack 135 SMs vs 120
+// for 8.  Results are cached per (device, dtype, B, n, flavour).
+Geometry score_geometry(int elem_bytes, int64_t B, int64_t n, int flavour) {
+  Geometry g;
+  const int vec = 16 / elem_bytes;
+  const VariantTable& tab = kCutmaxTables[elem_bytes == 8 ? 1 : 0];
+  const int oi = elem_bytes == 8 ? 1 : 0;
+  const int fntg = g_ovr.ntg[oi].load(), fe = g_ovr.e[oi].load(), fc = g_ovr.c[oi].load(), fmb = g_ovr.minb[oi].load();
+  if (fntg > 0) {  // pam_set_geometry_override
+    for (int i = 0; i < tab.count; ++i) {
+      const Variant& v = tab.v[i];
+      if (v.ntg == fntg && v.e == fe && v.minb == fmb && v.fn[flavour]) {
+        const int64_t L = slice_len(n, fc, vec);
+        if ((int64_t)v.ntg * v.e >= L) {
+          g.var = &v;
+          g.C = fc;
+          g.L = (int)L;
+        }
+        return g;
+      }
+    }
+    return g;
+  }
+  const int dev = current_device();
+  int nsm = 148;
+  if (dev >= 0 && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
+  const double a_us = elem_bytes == 8 ? 4.8 : 2.5, b_ns = elem_bytes == 8 ? 0.33 : 0.35;
+  double best_score = -1.0;
+  for (int C = 1; C <= 16; ++C) {
+    const int64_t L = slice_len(n, C, vec);
+    for (int i = 0; i < tab.count; ++i) {
+      const Variant& v = tab.v[i];
+      if (!v.fn[flavour]) continue;
+      const int64_t cap = (int64_t)v.ntg * v.e;
+      if (cap < L || (C > 1 && cap > L + L * 3 / 10 && flavour != 2)) continue;
+      if (C > 1 && L < 2048) continue;  // tiny slices: exchanges would dominate
+      const int smem = smem_bytes(v);
+      if (smem > 227 * 1024) continue;
+      const int active = dev >= 0 ? max_active_clusters(v.fn[flavour], v.ntg, C, smem) : nsm / C;
+      if (active <= 0) continue;
+      const int64_t clusters = (B < active) ? B : active;
+      const int64_t k = (clusters * C + nsm - 1) / nsm;
+      const double t_us = a_us + 1e-3 * b_ns * (double)cap * (double)(k < 1 ? 1 : k);
+      const double score = (double)clusters / t_us - 1e-9 * (double)C;  // tie-break: smaller clusters
+      if (score > best_score) { best_score = score; g.var = &v; g.C = C; g.L = (int)L; }
+    }
+  }
+  cudaGetLastError();
+  return g;
+}
+
+struct GeoKey {
+  int dev, elem_bytes, flavour, gen;
+  int64_t B, n;
+  bool operator==(const GeoKey& o) const {
+    return dev == o.dev && elem_bytes == o.elem_bytes && flavour == o.flavour && gen == o.gen && B == o.B && n == o.n;
+  }
+};
+struct GeoKeyHash {
+  size_t operator()(const GeoKey& k) const {
+    return std::hash<int64_t>()(k.B * 1000003 + k.n) ^ ((size_t)k.dev << 40) ^ ((size_t)k.elem_bytes << 48) ^
+           ((size_t)k.flavour << 52) ^ ((size_t)k.gen << 56);
+  }
+};
+std::mutex g_geo_mu;
+std::unordered_map<GeoKey, Geometry, GeoKeyHash> g_geo_cache;
+
+Geometry choose_geometry(int elem_bytes, int64_t B, int64_t n, int flavour) {
+  const GeoKey key{current_device(), elem_bytes, flavour, g_ovr.generation.load(), B, n};
+  {
+    std::lock_guard<std::mutex> lk(g_geo_mu);
+    auto it = g_geo_cache.find(key);
+    if (it != g_geo_cache.end()) return it->second;
+  }
+  const Geometry g = score_geometry(elem_bytes, B, n, flavour);
+  std::lock_guard<std::mutex> lk(g_geo_mu);
+  if (g_geo_cache.size() > 4096) g_geo_cache.clear();  // bounded
+  g_geo_cache.emplace(key, g);
+  return g;
 }
 
 int launch_cluster_kernel(const void* fn, int nt, int C, int clusters, int smem, cudaStream_t stream, void* kargs) {
@@ -192,6 +252,7 @@ int fill_row_params(const pam_cutmax_params* prm, RowParams* rp) {
   rp->invsqrt_mode = prm->invsqrt_mode;
   rp->inv_mode = prm->inv_mode;
   rp->eps_var = prm->eps_var;
+  rp->eps_stop = prm->eps_stop;
   for (int t = 0; t < prm->T; ++t) {
     rp->p[t] = prm->p[t];
     rp->inv_c[t] = 1.0 / prm->c[t];
@@ -203,82 +264,6 @@ int fill_row_params(const pam_cutmax_params* prm, RowParams* rp) {
   return PAM_OK;
 }
 
-// Geometry of the two-iterations-per-exchange kernel (cutmax_ahead_kernel.cuh).
-// Same scoring as choose_geometry: rows per microsecond = clusters / t_row with
-// t_row ~= a + b * cap * k; a (two exchanges + chains per row) = 2.6 us,
-// b ~= 36 fp64 instructions per element slot at 64/clk/SM = 0.33 ns.
-// Dev override: PAM_FORCE_AHEAD = "NTG,E,C".
-struct AheadGeometry {
-  const AheadVariant* var = nullptr;
-  int C = 0, L = 0;
-};
-int ahead_smem_bytes(const AheadVariant& v) { return ((v.ntg * v.e * 8 + 127) / 128) * 128 + v.ctl_bytes; }
-
-AheadGeometry choose_ahead_geometry(int64_t B, int64_t n) {
-  AheadGeometry g;
-  if (const char* fs = getenv("PAM_FORCE_AHEAD")) {
-    int ntg = 0, e = 0, c = 0;
-    if (sscanf(fs, "%d,%d,%d", &ntg, &e, &c) == 3) {
-      for (int i = 0; i < kNumAheadVariants; ++i) {
-        const AheadVariant& v = kAheadVariants[i];
-        const int64_t L = slice_len(n, c, 2);
-        if (v.ntg == ntg && v.e == e && (int64_t)v.ntg * v.e >= L) {
-          g.var = &v;
-          g.C = c;
-          g.L = (int)L;
-          return g;
-        }
-      }
-    }
-  }
-  int dev = 0;
-  const bool have_gpu = cudaGetDevice(&dev) == cudaSuccess;
-  int nsm = 148;
-  if (have_gpu && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
-  const double a_us = 2.6, b_ns = 0.33;
-  double best_score = -1.0;
-  for (int C = 1; C <= 16; ++C) {
-    const int64_t L = slice_len(n, C, 2);
-    for (int i = 0; i < kNumAheadVariants; ++i) {
-      const AheadVariant& v = kAheadVariants[i];
-      const int64_t cap = (int64_t)v.ntg * v.e;
-      if (cap < L || (C > 1 && cap > L + L * 3 / 10)) continue;
-      if (C > 1 && L < 2048) continue;
-      const int smem = ahead_smem_bytes(v);
-      if (smem > 227 * 1024) continue;
-      const int active = have_gpu ? max_active_clusters(v.fn, v.ntg, C, smem) : nsm / C;
-      if (active <= 0) continue;
-      const int64_t clusters = (B < active) ? B : active;
-      const int64_t k = (clusters * C + nsm - 1) / nsm;
-      const double t_us = a_us + 1e-3 * b_ns * (double)cap * (double)(k < 1 ? 1 : k);
-      const double score = (double)clusters / t_us - 1e-9 * (double)C;
-      if (score > best_score) {
-        best_score = score;
-        g.var = &v;
-        g.C = C;
-        g.L = (int)L;
-      }
-    }
-  }
-  cudaGetLastError();
-  return g;
-}
-
-// The ahead kernel serves fp64, p = 3 everywhere, exact scalars, normalised
-// output without the stats side output, on TMA-aligned rows.
-bool ahead_eligible(const pam_cutmax_params* prm, bool tma, const double* d_stats) {
-  // Opt-in until it beats cutmax_rows_kernel on the headline shape:
-  // PAM_ENABLE_AHEAD=1 (or PAM_FORCE_AHEAD=NTG,E,C) selects it.
-  if (!getenv("PAM_ENABLE_AHEAD") && !getenv("PAM_FORCE_AHEAD")) return false;
-  if (!tma || d_stats || getenv("PAM_DISABLE_AHEAD") || getenv("PAM_FORCE_CFG_F64") || getenv("PAM_FORCE_GENERIC_P"))
-    return false;
-  if (prm->flags & PAM_F_NO_NORMALIZE) return false;
-  if (prm->invsqrt_mode != PAM_MODE_EXACT || prm->inv_mode != PAM_MODE_EXACT) return false;
-  for (int t = 0; t < prm->T; ++t)
-    if (prm->p[t] != 3) return false;
-  return true;
-}
-
 template <typename Elem>
 int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const pam_cutmax_params* prm, Elem* d_z,
                       int64_t ld_z, int32_t* d_argmax, int32_t* d_status, double* d_stats, cudaStream_t stream) {
@@ -286,45 +271,15 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   int st = pam_validate_cutmax_params(prm, n);
   if (st) return st;
   if (B < 0 || ld_x < n || ld_z < n || (B > 0 && (!d_x || !d_z))) return PAM_ERR_BAD_ARGUMENT;
-  if (prm->eps_stop > 0.0) return PAM_ERR_UNSUPPORTED;
   if (B == 0) return PAM_OK;
   if (n > (int64_t)1 << 30) return PAM_ERR_UNSUPPORTED;
   const int vec = 16 / (int)sizeof(Elem);
   const bool tma = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_z % 16 == 0) && (ld_x % vec == 0) &&
-                   (ld_z % vec == 0) && (n % vec == 0) && getenv("PAM_DISABLE_TMA") == nullptr;
-  if (sizeof(Elem) == 8 && ahead_eligible(prm, tma, d_stats)) {
-    const AheadGeometry ag = choose_ahead_geometry(B, n);
-    if (ag.var) {
-      const int smem = ahead_smem_bytes(*ag.var);
-      const int maxcl = max_active_clusters(ag.var->fn, ag.var->ntg, ag.C, smem);
-      if (maxcl <= 0) return cuda_fail(cudaErrorInvalidConfiguration, "no cluster fits (occupancy 0)");
-      const int clusters = (int)(B < maxcl ? B : maxcl);
-      CutmaxArgs ka;
-      memset(&ka, 0, sizeof ka);
-      ka.x = d_x;
-      ka.z = d_z;
-      ka.argmax = d_argmax;
-      ka.status = d_status;
-      ka.ldx = ld_x;
-      ka.ldz = ld_z;
-      ka.B = B;
-      ka.n = n;
-      ka.L = ag.L;
-      ka.ctrl_offset = ((ag.var->ntg * ag.var->e * 8 + 127) / 128) * 128;
-      ka.tma = 1;
-      ka.inv_n = 1.0 / (double)n;
-      const char* df = getenv("PAM_DEBUG_FLAGS");
-      ka.debug_flags = df ? atoi(df) : 0;
-      fill_row_params(prm, &ka.rp);
-      if (g_trace && (int64_t)clusters * ag.C * kTraceRows * kTraceEvents <= g_trace_entries) ka.trace = g_trace;
-      return launch_cluster_kernel(ag.var->fn, ag.var->ntg, ag.C, clusters, smem, stream, &ka);
-    }
-  }
-  const Geometry g = choose_geometry((int)sizeof(Elem), B, n);
+                   (ld_z % vec == 0) && (n % vec == 0);
+  const int flavour = flavour_of(prm);
+  const Geometry g = choose_geometry((int)sizeof(Elem), B, n, flavour);
   if (!g.var) return PAM_ERR_UNSUPPORTED;
-  bool p3 = getenv("PAM_FORCE_GENERIC_P") == nullptr;  // dev knob: A/B the generic-p kernel
-  for (int t = 0; t < prm->T; ++t) p3 = p3 && (prm->p[t] == 3);
-  const void* fn = g.var->fn[p3 ? 1 : 0];
+  const void* fn = g.var->fn[flavour];
   // the row buffer is sized for the full capacity even without TMA so the
   // occupancy (and the chooser's estimate) does not depend on alignment
   const int smem = smem_bytes(*g.var);
@@ -347,10 +302,6 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   ka.ctrl_offset = buffer_bytes(*g.var);
   ka.tma = tma ? 1 : 0;
   ka.inv_n = 1.0 / (double)n;
-  {
-    const char* df = getenv("PAM_DEBUG_FLAGS");
-    ka.debug_flags = df ? atoi(df) : 0;
-  }
   if (g_trace && (int64_t)clusters * g.C * kTraceRows * kTraceEvents <= g_trace_entries) ka.trace = g_trace;
   fill_row_params(prm, &ka.rp);
   return launch_cluster_kernel(fn, nt, g.C, clusters, smem, stream, &ka);
@@ -363,7 +314,6 @@ int sampler_batch_impl(const double* d_x, int64_t ld_x, int64_t B, int64_t n, co
   int st = pam_validate_cutmax_params(prm, n);
   if (st) return st;
   if (B < 0 || ld_x < n || (B > 0 && !d_x) || (d_onehot && ld_onehot < n)) return PAM_ERR_BAD_ARGUMENT;
-  if (prm->eps_stop > 0.0) return PAM_ERR_UNSUPPORTED;
   if (!(cfg->p > 0.0 && cfg->p < 1.0)) return PAM_ERR_DOMAIN;
   double alpha = cfg->alpha;
   if (!gumbel && !(alpha > 0.0)) {
@@ -384,9 +334,8 @@ int sampler_batch_impl(const double* d_x, int64_t ld_x, int64_t B, int64_t n, co
     if (var) C = c;
   }
   if (!var) return PAM_ERR_UNSUPPORTED;
-  bool p3 = true;
-  for (int t = 0; t < prm->T; ++t) p3 = p3 && (prm->p[t] == 3);
-  const void* fn = var->fn[p3 ? 1 : 0][gumbel ? 1 : 0];
+  const int flavour = flavour_of(prm);
+  const void* fn = flavour == 2 ? var->stop[gumbel ? 1 : 0] : var->fn[flavour][gumbel ? 1 : 0];
   const int buf_bytes = (int)(((L * 8) + 127) / 128 * 128);
   const int smem = buf_bytes + (int)sizeof(ControlBlock);
   const int maxcl = max_active_clusters(fn, var->nt, C, smem);
@@ -410,7 +359,7 @@ int sampler_batch_impl(const double* d_x, int64_t ld_x, int64_t B, int64_t n, co
   sa.seed = cfg->seed;
   sa.draw = cfg->draw;
   sa.inv_n = 1.0 / (double)n;
-  sa.tma = ((uintptr_t)d_x % 16 == 0) && (ld_x % 2 == 0) && (n % 2 == 0) && getenv("PAM_DISABLE_TMA") == nullptr;
+  sa.tma = ((uintptr_t)d_x % 16 == 0) && (ld_x % 2 == 0) && (n % 2 == 0);
   fill_row_params(prm, &sa.rp);
   if (g_trace && (int64_t)clusters * C * kTraceRows * kTraceEvents <= g_trace_entries) sa.trace = g_trace;
   return launch_cluster_kernel(fn, var->nt, C, clusters, smem, stream, &sa);
@@ -466,14 +415,38 @@ int analysis_impl(bool jvp, const double* d_x, const double* d_v, int64_t ld_x, 
 }
 
 // ---------------------------------------------------- host-buffer e2e path
+// Device staging for the host-pointer entry points: three pipeline slots
+// (H2D -> kernel -> D2H, one stream each).  Workspaces are pooled per device:
+// a call takes a free one (or creates one) and returns it, so concurrent host
+// calls do not serialise on a global lock, and switching devices never drops a
+// live allocation.  Workspaces live for the process.
 struct HostWorkspace {
-  std::mutex mu;
+  int dev = -1;
   void* dbuf = nullptr;
   size_t cap = 0;
   cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
-  int dev = -1;
 };
-HostWorkspace g_ws;
+std::mutex g_ws_mu;
+std::vector<HostWorkspace*> g_ws_free;  // idle workspaces of every device
+
+HostWorkspace* ws_acquire(int dev) {
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (size_t i = 0; i < g_ws_free.size(); ++i)
+      if (g_ws_free[i]->dev == dev) {
+        HostWorkspace* w = g_ws_free[i];
+        g_ws_free.erase(g_ws_free.begin() + (long)i);
+        return w;
+      }
+  }
+  HostWorkspace* w = new HostWorkspace();
+  w->dev = dev;
+  return w;
+}
+void ws_release(HostWorkspace* w) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  g_ws_free.push_back(w);
+}
 
 template <typename Elem>
 int cutmax_host_impl(const Elem* h_x, int64_t B, int64_t n, const pam_cutmax_params* prm, Elem* h_z,
@@ -482,48 +455,53 @@ int cutmax_host_impl(const Elem* h_x, int64_t B, int64_t n, const pam_cutmax_par
   int st = pam_validate_cutmax_params(prm, n);
   if (st) return st;
   if (B == 0) return PAM_OK;
-  std::lock_guard<std::mutex> lk(g_ws.mu);
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (g_ws.dev != dev) {
-    for (auto& s : g_ws.streams) s = nullptr;
-    g_ws.dbuf = nullptr;
-    g_ws.cap = 0;
-    g_ws.dev = dev;
-  }
-  for (auto& s : g_ws.streams)
+  const int dev = current_device();
+  if (dev < 0) return cuda_fail(cudaErrorNoDevice, "cudaGetDevice");
+  HostWorkspace* ws = ws_acquire(dev);
+  struct Release {
+    HostWorkspace* w;
+    ~Release() { ws_release(w); }
+  } release{ws};
+  for (auto& s : ws->streams)
     if (!s) {
       cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
       if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
     }
   const size_t row_bytes = (size_t)n * sizeof(Elem);
   // chunk: ~128 MiB of input per chunk, 3 chunks in flight (PCIe-bound either way: 32 MiB gave
-  // 35.5k rows/s, 128 MiB 37.8k at 4096 x 151936 fp64; dev knob PAM_HOST_CHUNK_MB)
-  size_t chunk_mb = 128;
-  if (const char* e = getenv("PAM_HOST_CHUNK_MB")) chunk_mb = (size_t)atoi(e) > 0 ? (size_t)atoi(e) : 128;
-  int64_t rows_per_chunk = (int64_t)((chunk_mb << 20) / row_bytes);
+  // 35.5k rows/s, 128 MiB 37.8k at 4096 x 151936 fp64; pam_set_host_chunk_bytes overrides)
+  const int64_t chunk_bytes = g_ovr.host_chunk_bytes.load();
+  int64_t rows_per_chunk = (int64_t)((size_t)chunk_bytes / row_bytes);
   if (rows_per_chunk < 1) rows_per_chunk = 1;
   if (rows_per_chunk > B) rows_per_chunk = B;
-  const size_t per_slot = rows_per_chunk * (2 * row_bytes + 2 * sizeof(int32_t)) + 256;
+  // every sub-buffer starts on a 256-byte boundary, so the kernel keeps its TMA path
+  auto up256 = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t xz_bytes = up256(rows_per_chunk * row_bytes);
+  const size_t i32_bytes = up256(rows_per_chunk * sizeof(int32_t));
+  const size_t per_slot = 2 * xz_bytes + 2 * i32_bytes;
   const size_t need = 3 * per_slot;
-  if (g_ws.cap < need) {
-    if (g_ws.dbuf) cudaFree(g_ws.dbuf);
-    g_ws.dbuf = nullptr;
-    cudaError_t e = cudaMalloc(&g_ws.dbuf, need);
-    if (e != cudaSuccess) { g_ws.cap = 0; return cuda_fail(e, "cudaMalloc workspace"); }
-    g_ws.cap = need;
+  if (ws->cap < need) {
+    if (ws->dbuf) {
+      for (auto& s : ws->streams) cudaStreamSynchronize(s);
+      cudaFree(ws->dbuf);
+    }
+    ws->dbuf = nullptr;
+    ws->cap = 0;
+    cudaError_t e = cudaMalloc(&ws->dbuf, need);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc workspace");
+    ws->cap = need;
   }
   int rc = PAM_OK;
   int64_t chunk = 0;
   for (int64_t r0 = 0; r0 < B; r0 += rows_per_chunk, ++chunk) {
     const int64_t rows = (B - r0) < rows_per_chunk ? (B - r0) : rows_per_chunk;
     const int slot = (int)(chunk % 3);
-    cudaStream_t s = g_ws.streams[slot];
-    char* base = (char*)g_ws.dbuf + slot * per_slot;
+    cudaStream_t s = ws->streams[slot];
+    char* base = (char*)ws->dbuf + slot * per_slot;
     Elem* dx = (Elem*)base;
-    Elem* dz = (Elem*)(base + rows_per_chunk * row_bytes);
-    int32_t* dam = (int32_t*)(base + 2 * rows_per_chunk * row_bytes);
-    int32_t* dst = dam + rows_per_chunk;
+    Elem* dz = (Elem*)(base + xz_bytes);
+    int32_t* dam = (int32_t*)(base + 2 * xz_bytes);
+    int32_t* dst = (int32_t*)(base + 2 * xz_bytes + i32_bytes);
     cudaError_t e = cudaMemcpyAsync(dx, h_x + r0 * n, rows * row_bytes, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
     rc = cutmax_batch_impl<Elem>(dx, n, rows, n, prm, dz, n, dam, dst, nullptr, s);
@@ -535,7 +513,7 @@ int cutmax_host_impl(const Elem* h_x, int64_t B, int64_t n, const pam_cutmax_par
       e = cudaMemcpyAsync(h_status + r0, dst, rows * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "D2H"); break; }
   }
-  for (auto& s : g_ws.streams) {
+  for (auto& s : ws->streams) {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess && rc == PAM_OK) rc = cuda_fail(e, "cudaStreamSynchronize");
   }
@@ -703,29 +681,10 @@ int pam_cutmax_jvp_batch_f64(const double* d_x, const double* d_v, int64_t ld_x,
 int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_params* prm, pam_launch_info* info) {
   if (!info || (dtype_bytes != 4 && dtype_bytes != 8)) return PAM_ERR_BAD_ARGUMENT;
   memset(info, 0, sizeof *info);
-  if (dtype_bytes == 8 && prm && n % 2 == 0 && ahead_eligible(prm, true, nullptr)) {
-    const AheadGeometry ag = choose_ahead_geometry(B, n);
-    if (ag.var) {
-      const int smem = ahead_smem_bytes(*ag.var);
-      info->threads = ag.var->ntg;
-      info->elems_per_thread = ag.var->e;
-      info->cluster = ag.C;
-      info->smem_bytes = smem;
-      info->tma = 1;
-      const int maxcl = max_active_clusters(ag.var->fn, ag.var->ntg, ag.C, smem);
-      info->clusters = (int)(B < maxcl ? B : maxcl);
-      info->ctas = info->clusters * ag.C;
-      info->groups = 1;
-      info->kernel_id = 1000 + (int)(ag.var - kAheadVariants);  // 1000+: the two-iterations-per-exchange kernel
-      return PAM_OK;
-    }
-  }
-  const Geometry g = choose_geometry(dtype_bytes, B, n);
+  const int flavour = prm ? flavour_of(prm) : 1;
+  const Geometry g = choose_geometry(dtype_bytes, B, n, flavour);
   if (!g.var) return PAM_ERR_UNSUPPORTED;
-  bool p3 = true;
-  if (prm)
-    for (int t = 0; t < prm->T; ++t) p3 = p3 && (prm->p[t] == 3);
-  const void* fn = g.var->fn[p3 ? 1 : 0];
+  const void* fn = g.var->fn[flavour];
   const int smem = smem_bytes(*g.var);
   info->threads = g.var->ntg;
   info->elems_per_thread = g.var->e;
@@ -736,7 +695,32 @@ int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_par
   info->clusters = (int)(B < maxcl ? B : maxcl);
   info->ctas = info->clusters * g.C;
   info->groups = 1;
-  info->kernel_id = (int)(g.var - kCutmaxVariants);
+  const VariantTable& tab = kCutmaxTables[dtype_bytes == 8 ? 1 : 0];
+  info->kernel_id = (int)(g.var - tab.v) + 100 * flavour;
+  return PAM_OK;
+}
+
+int pam_set_geometry_override(int dtype_bytes, int threads, int elems_per_thread, int cluster, int min_blocks) {
+  if (dtype_bytes != 4 && dtype_bytes != 8) return PAM_ERR_BAD_ARGUMENT;
+  const int oi = dtype_bytes == 8 ? 1 : 0;
+  if (threads > 0) {
+    if (cluster < 1 || cluster > 16 || elems_per_thread < 1) return PAM_ERR_BAD_ARGUMENT;
+    bool found = false;
+    const VariantTable& tab = kCutmaxTables[oi];
+    for (int i = 0; i < tab.count; ++i)
+      found = found || (tab.v[i].ntg == threads && tab.v[i].e == elems_per_thread && tab.v[i].minb == min_blocks);
+    if (!found) return PAM_ERR_UNSUPPORTED;
+  }
+  g_ovr.ntg[oi] = threads > 0 ? threads : 0;
+  g_ovr.e[oi] = elems_per_thread;
+  g_ovr.c[oi] = cluster;
+  g_ovr.minb[oi] = min_blocks;
+  g_ovr.generation.fetch_add(1);
+  return PAM_OK;
+}
+
+int pam_set_host_chunk_bytes(int64_t bytes) {
+  g_ovr.host_chunk_bytes = bytes > 0 ? bytes : (128ll << 20);
   return PAM_OK;
 }
 

@@ -1,13 +1,23 @@
 // pam_variants.h — the compiled kernel instantiations the launcher can pick
 // from.  Each table lives in its own translation unit so nvcc builds them in
-// parallel.
+// parallel; the launcher walks kCutmaxTables.
 #pragma once
 
 namespace pam {
 
+// One CutMax geometry: threads per CTA, elements per thread, launch-bounds
+// min blocks (0: auto), and its kernels:
+//   fn[0] generic p (runtime schedule), fn[1] p = 3 everywhere (analytic
+//   normaliser), fn[2] generic p with early stopping (eps_stop > 0; nullptr
+//   when this geometry has no such instantiation).
 struct Variant {
-  int elem_bytes, ntg, e, minb;  // threads per CTA, elements per thread, launch-bounds min blocks (0: auto)
-  const void* fn[2];          // [P==3]
+  int elem_bytes, ntg, e, minb;
+  const void* fn[3];
+};
+
+struct VariantTable {
+  const Variant* v;
+  int count;
 };
 
 // Analysis kernels (analysis_kernel.cuh): convergence trace and forward-mode JVP.
@@ -20,19 +30,13 @@ struct AnalysisVariant {
 struct SamplerVariant {
   int nt, e;
   const void* fn[2][2];  // [P==3][GUMBEL]
+  const void* stop[2];   // generic p with early stopping, [GUMBEL]
 };
 
-// Two-iterations-per-exchange fp64 p = 3 kernel (cutmax_ahead_kernel.cuh).
-struct AheadVariant {
-  int ntg, e;
-  int ctl_bytes;  // sizeof(AhCtl<ntg>)
-  const void* fn;
-};
-
-extern const Variant kCutmaxVariants[];
-extern const AheadVariant kAheadVariants[];
-extern const int kNumAheadVariants;
-extern const int kNumCutmaxVariants;
+extern const Variant kCutmaxVariantsF64[];
+extern const int kNumCutmaxVariantsF64;
+extern const Variant kCutmaxVariantsF32[];
+extern const int kNumCutmaxVariantsF32;
 extern const AnalysisVariant kAnalysisVariants[];
 extern const int kNumAnalysisVariants;
 extern const SamplerVariant kSamplerVariants[];

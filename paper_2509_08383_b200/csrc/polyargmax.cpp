@@ -210,6 +210,7 @@ ScoreVector cutmax(const LogitVector& x, const CutMaxParams& params) {
   throw_status(rc, 0);
   throw_status(st, 0);
   out.argmax = am;
+  out.tieWarning = (st & PAM_ROW_FLAG_TIE) != 0;
   return out;
 }
 
@@ -282,6 +283,7 @@ static SampleOutcome sample_one(const LogitVector& x, const pam_sampler_cfg& cfg
   throw_status(st, 0);
   out.tokenIndex = tok;
   out.insideNucleus = ins != 0;
+  out.tieWarning = (st & PAM_ROW_FLAG_TIE) != 0;
   return out;
 }
 

@@ -1,4 +1,4 @@
-// sampler_variants.cu — instantiations of sampler_rows_kernel<NT, E, P, GUMBEL>.
+// sampler_variants.cu — instantiations of sampler_rows_kernel<NT, E, P, GUMBEL, STOP>.
 #include "nucleus_kernel.cuh"
 #include "pam_variants.h"
 
@@ -6,9 +6,12 @@ namespace pam {
 
 #define PAM_SAMPLER_VARIANT(NT, E)                                                                             \
   {                                                                                                            \
-    NT, E, {                                                                                                   \
-      {(const void*)sampler_rows_kernel<NT, E, 0, false>, (const void*)sampler_rows_kernel<NT, E, 0, true>},   \
-          {(const void*)sampler_rows_kernel<NT, E, 3, false>, (const void*)sampler_rows_kernel<NT, E, 3, true>} \
+    NT, E,                                                                                                     \
+        {{(const void*)sampler_rows_kernel<NT, E, 0, false>, (const void*)sampler_rows_kernel<NT, E, 0, true>},  \
+         {(const void*)sampler_rows_kernel<NT, E, 3, false>, (const void*)sampler_rows_kernel<NT, E, 3, true>}}, \
+    {                                                                                                          \
+      (const void*)sampler_rows_kernel<NT, E, 0, false, true>,                                                 \
+          (const void*)sampler_rows_kernel<NT, E, 0, true, true>                                               \
     }                                                                                                          \
   }
 

@@ -80,3 +80,8 @@ def raise_for_status(status: int, row: int = 0, what: str = "") -> None:
     if s in (_abi.PAM_ERR_DEGENERATE_INPUT, _abi.PAM_ERR_RANGE, _abi.PAM_ERR_SINGULAR):
         msg += f" (row {row})"
     raise cls(msg)
+
+
+class TieWarning(UserWarning):
+    """TieWarning: the input's top-2 gap is below 1e-9.  Reported,
+    never raised as an error: rows carry the PAM_ROW_FLAG_TIE bit in their status."""

@@ -27,7 +27,9 @@ from typing import Optional, Sequence, Union
 import numpy as np
 
 from . import _abi
-from .errors import DomainError, InvalidParamsError, raise_for_status
+import warnings
+
+from .errors import DomainError, InvalidParamsError, TieWarning, raise_for_status
 
 _lib = _abi.load()
 
@@ -124,11 +126,13 @@ class CutMaxParams:
 
 @dataclass
 class ScoreVector:
-    """ScoreVector plus the argmax computed by the kernel."""
+    """ScoreVector plus the argmax computed by the kernel and the
+    TieWarning flag."""
 
     values: np.ndarray
     normalized: bool
     argmax: int
+    tieWarning: bool = False
 
 
 @dataclass
@@ -252,8 +256,11 @@ def cutmax_batch(X, params: Optional[CutMaxParams] = None, raise_on_error: bool 
 def cutmax(x, params: Optional[CutMaxParams] = None) -> ScoreVector:
     """cutmax(x, params) -> ScoreVector (SPEC.md:60-69)."""
     params = params or CutMaxParams()
-    z, am, _ = cutmax_batch(np.asarray(x, dtype=np.float64)[None, :], params)
-    return ScoreVector(values=z[0], normalized=params.normalize, argmax=int(am[0]))
+    z, am, st = cutmax_batch(np.asarray(x, dtype=np.float64)[None, :], params)
+    tie = bool(int(st[0]) & _abi.PAM_ROW_FLAG_TIE)
+    if tie:
+        warnings.warn("cutmax: top-2 gap of the input < 1e-9 (SPEC.md:122)", TieWarning, stacklevel=2)
+    return ScoreVector(values=z[0], normalized=params.normalize, argmax=int(am[0]), tieWarning=tie)
 
 
 # --------------------------------------------------------- device API ------
@@ -265,10 +272,32 @@ def _torch():
     return torch
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, device):
+    """The launch stream: the caller's (it must belong to `device`) or the
+    current stream of `device` (not of the current device)."""
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return C.c_void_p(s.cuda_stream)
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    elif stream.device != device:
+        raise InvalidParamsError(f"stream is on {stream.device}, tensors on {device}")
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _check_out(t, name, device, dtype, shape, contiguous=False):
+    """Caller-supplied output buffers: same device, dtype and shape as the call
+    writes, unit stride along rows (and fully contiguous where the kernel
+    indexes it flat), so the kernel can never write out of bounds."""
+    if t.device != device:
+        raise InvalidParamsError(f"{name} is on {t.device}, x on {device}")
+    if t.dtype != dtype:
+        raise InvalidParamsError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise InvalidParamsError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if t.dim() > 0 and t.stride(-1) != 1:
+        raise InvalidParamsError(f"{name} must have unit stride along its last dimension")
+    if contiguous and not t.is_contiguous():
+        raise InvalidParamsError(f"{name} must be contiguous")
+    return t
 
 
 def cutmax_batch_device(x, params: Optional[CutMaxParams] = None, z=None, argmax=None, status=None,
@@ -282,25 +311,29 @@ def cutmax_batch_device(x, params: Optional[CutMaxParams] = None, z=None, argmax
     params = params or CutMaxParams()
     if x.dim() != 2 or not x.is_cuda:
         raise InvalidParamsError("x must be a 2-D CUDA tensor")
+    if x.dtype not in (torch.float64, torch.float32):
+        raise InvalidParamsError("dtype must be float64 or float32")
     B, n = x.shape
     ld = x.stride(0)
     if x.stride(1) != 1:
         raise InvalidParamsError("rows must be contiguous")
+    dev = x.device
     if z is None:
-        z = torch.empty((B, n), dtype=x.dtype, device=x.device)
+        z = torch.empty((B, n), dtype=x.dtype, device=dev)
+    _check_out(z, "z", dev, x.dtype, (B, n))
     if argmax is None:
-        argmax = torch.empty(B, dtype=torch.int32, device=x.device)
+        argmax = torch.empty(B, dtype=torch.int32, device=dev)
+    _check_out(argmax, "argmax", dev, torch.int32, (B,))
     if status is None:
-        status = torch.empty(B, dtype=torch.int32, device=x.device)
+        status = torch.empty(B, dtype=torch.int32, device=dev)
+    _check_out(status, "status", dev, torch.int32, (B,))
+    if stats is not None:
+        _check_out(stats, "stats", dev, torch.float64, (B, int(params.T), 2), contiguous=True)
     prm = params.lower()
-    if x.dtype == torch.float64:
-        fn = _lib.pam_cutmax_batch_f64
-    elif x.dtype == torch.float32:
-        fn = _lib.pam_cutmax_batch_f32
-    else:
-        raise InvalidParamsError("dtype must be float64 or float32")
-    rc = fn(x.data_ptr(), ld, B, n, C.byref(prm), z.data_ptr(), z.stride(0), argmax.data_ptr(),
-            status.data_ptr(), stats.data_ptr() if stats is not None else None, _stream_ptr(stream))
+    fn = _lib.pam_cutmax_batch_f64 if x.dtype == torch.float64 else _lib.pam_cutmax_batch_f32
+    with torch.cuda.device(dev):  # the C ABI launches on the current device
+        rc = fn(x.data_ptr(), ld, B, n, C.byref(prm), z.data_ptr(), z.stride(0), argmax.data_ptr(),
+                status.data_ptr(), stats.data_ptr() if stats is not None else None, _stream_ptr(stream, dev))
     raise_for_status(rc, what="cutmax_batch_device")
     return z, argmax, status
 
@@ -309,16 +342,22 @@ def _sample_device(fn_name, x, cfg: SamplerConfig, params: CutMaxParams, onehot=
     torch = _torch()
     if x.dim() != 2 or not x.is_cuda or x.dtype != torch.float64:
         raise InvalidParamsError("x must be a 2-D float64 CUDA tensor")
+    if x.stride(1) != 1:
+        raise InvalidParamsError("rows must be contiguous")
     B, n = x.shape
-    token = torch.empty(B, dtype=torch.int32, device=x.device)
-    inside = torch.empty(B, dtype=torch.uint8, device=x.device)
-    status = torch.empty(B, dtype=torch.int32, device=x.device)
+    dev = x.device
+    token = torch.empty(B, dtype=torch.int32, device=dev)
+    inside = torch.empty(B, dtype=torch.uint8, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    if onehot is not None:
+        _check_out(onehot, "onehot", dev, torch.float64, (B, n))
     c = cfg.lower()
     prm = params.lower()
-    rc = getattr(_lib, fn_name)(x.data_ptr(), x.stride(0), B, n, C.byref(c), C.byref(prm), token.data_ptr(),
-                                inside.data_ptr(), onehot.data_ptr() if onehot is not None else None,
-                                onehot.stride(0) if onehot is not None else 0, status.data_ptr(),
-                                _stream_ptr(stream))
+    with torch.cuda.device(dev):
+        rc = getattr(_lib, fn_name)(x.data_ptr(), x.stride(0), B, n, C.byref(c), C.byref(prm), token.data_ptr(),
+                                    inside.data_ptr(), onehot.data_ptr() if onehot is not None else None,
+                                    onehot.stride(0) if onehot is not None else 0, status.data_ptr(),
+                                    _stream_ptr(stream, dev))
     raise_for_status(rc, what=fn_name)
     return token, inside, status
 
@@ -366,13 +405,16 @@ def convergence_trace_batch_device(x, params: Optional[CutMaxParams] = None, str
     if x.dim() != 2 or not x.is_cuda or x.dtype != torch.float64:
         raise InvalidParamsError("x must be a 2-D float64 CUDA tensor")
     params = params or CutMaxParams()
+    if x.stride(1) != 1:
+        raise InvalidParamsError("rows must be contiguous")
     B, n = x.shape
     out = torch.zeros((B, params.T, 4), dtype=torch.float64, device=x.device)
     status = torch.empty(B, dtype=torch.int32, device=x.device)
     prm = params.lower()
-    raise_for_status(_lib.pam_convergence_trace_batch_f64(x.data_ptr(), x.stride(0), B, n, C.byref(prm),
-                                                          out.data_ptr(), status.data_ptr(), _stream_ptr(stream)),
-                     what="convergence_trace_batch_device")
+    with torch.cuda.device(x.device):
+        rc = _lib.pam_convergence_trace_batch_f64(x.data_ptr(), x.stride(0), B, n, C.byref(prm), out.data_ptr(),
+                                                  status.data_ptr(), _stream_ptr(stream, x.device))
+    raise_for_status(rc, what="convergence_trace_batch_device")
     return out, status
 
 
@@ -402,15 +444,18 @@ def cutmax_jvp_batch_device(x, v, params: Optional[CutMaxParams] = None, want_z:
     z = torch.empty_like(x) if want_z else None
     status = torch.empty(B, dtype=torch.int32, device=x.device)
     prm = params.lower()
-    raise_for_status(_lib.pam_cutmax_jvp_batch_f64(x.data_ptr(), v.data_ptr(), n, B, n, C.byref(prm),
-                                                   z.data_ptr() if z is not None else None, dz.data_ptr(), n,
-                                                   status.data_ptr(), _stream_ptr(stream)),
-                     what="cutmax_jvp_batch_device")
+    if v.device != x.device:
+        raise InvalidParamsError("x and v must be on one device")
+    with torch.cuda.device(x.device):
+        rc = _lib.pam_cutmax_jvp_batch_f64(x.data_ptr(), v.data_ptr(), n, B, n, C.byref(prm),
+                                           z.data_ptr() if z is not None else None, dz.data_ptr(), n,
+                                           status.data_ptr(), _stream_ptr(stream, x.device))
+    raise_for_status(rc, what="cutmax_jvp_batch_device")
     return z, dz, status
 
 
 def _check_rows(status):
-    st = status.cpu().numpy()
+    st = status.cpu().numpy() & 0xFF
     bad = np.nonzero(st)[0]
     if bad.size:
         raise_for_status(int(st[bad[0]]), row=int(bad[0]))
@@ -502,7 +547,7 @@ def violationExperiment(prompts, cfg: SamplerConfig, draws: int, params: Optiona
         c = SamplerConfig(p=cfg.p, q=cfg.q, alpha=cfg.alpha, seed=cfg.seed ^ i, draw=cfg.draw)
         for name, fn in (("betaCut", nucleus_sample_batch_device), ("gumbel", gumbel_sample_batch_device)):
             _, inside, st = fn(X, c, params)
-            st_h = st.cpu().numpy()
+            st_h = st.cpu().numpy() & 0xFF  # the TieWarning bit is not an error
             if np.any(st_h != 0):
                 raise_for_status(int(st_h[st_h != 0][0]), row=int(np.nonzero(st_h)[0][0]))
             rates[name].append(1.0 - float(inside.double().mean().item()))
@@ -543,3 +588,20 @@ def launch_info(dtype_bytes: int, B: int, n: int, params: Optional[CutMaxParams]
 
 def kernel_launch_count() -> int:
     return int(_lib.pam_kernel_launch_count())
+
+
+class geometry_override:
+    """Tuning / test hook: force the CutMax launch geometry for one dtype
+    (dtype_bytes 8 or 4) to a compiled variant (threads x elems per thread) and
+    a cluster size, for the duration of a ``with`` block (pam_set_geometry_override)."""
+
+    def __init__(self, dtype_bytes: int, threads: int, elems: int, cluster: int, min_blocks: int = 0):
+        self.args = (int(dtype_bytes), int(threads), int(elems), int(cluster), int(min_blocks))
+
+    def __enter__(self):
+        raise_for_status(_lib.pam_set_geometry_override(*self.args), what="geometry_override")
+        return self
+
+    def __exit__(self, *exc):
+        _lib.pam_set_geometry_override(self.args[0], 0, 0, 0, 0)
+        return False
