@@ -3,22 +3,29 @@
 
 Workload (N=1): C5's largest single-GPU point, B = 4096 rows x n = 151936 fp64
 logits, T = 4, p = 3, c = 5 (c pinned), N(0, 3^2) synthetic
-logits generated on the device from a fixed seed.  One step = one fused
-CutMax pass over the whole batch (read X, write Z + argmax + status).
-Inputs (4.98 GB) are far larger than the 126 MB L2, so no L2 flush is needed.
+logits from a fixed seed.  One step = one fused CutMax pass over the whole
+batch (read X, write Z + argmax + status).  The inputs (4.98 GB) are far larger
+than the 126 MB L2, so no L2 flush is needed between steps.
 
 `value` is whole-job rows/s with X resident in HBM; `e2e` is the same metric
 through the host-buffer C ABI (pam_cutmax_batch_host_f64: pinned H2D of X, the
-kernel, D2H of Z and argmax inside the timed region).  --impl reference times
-the CPU oracle (the restatement of the reference's algorithm; the reference
-ships no implementation) with all host threads on the same config.
+kernel, D2H of Z, argmax and status inside the timed region).
 
-Multi-GPU (torchrun): rows are independent, so every rank runs its own B-row
-batch (weak scaling, no data-path collective); time = max over ranks.
+--impl reference times the CPU oracle (oracle/liboracle.so: the plain-C
+restatement of the reference's algorithm -- the reference ships no
+implementation) on the same 4096-row config with every host
+thread.  That arm imports nothing from the product package.
+
+Multi-GPU: rows are independent, so every rank runs its own
+B-row batch (weak scaling, no data-path collective) and time = max over ranks.
+`--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks.
 """
 import argparse
 import json
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,24 +39,49 @@ N_VOCAB = 151936
 B_ROWS = 4096
 T_ITERS, P_POW, C_SCALE = 4, 3, 5.0
 SEED = 2509_08383
+WORKLOAD = f"C5 B={B_ROWS} x n={N_VOCAB} fp64, T=4, p=3, c=5"
+BYTES_PER_ROW = 2 * N_VOCAB * 8 + 4  # read x, write Z and the int32 argmax
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def gaussian_rows(rows: int, seed: int):
+    """Host copy of the workload's N(0, 3^2) rows (numpy, no product import)."""
+    import numpy as np
+
+    return np.random.default_rng(seed).normal(0.0, 3.0, size=(rows, N_VOCAB))
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    """DRAM bytes per launch of the benched kernel from the committed ncu capture."""
     try:
-        with open(p) as f:
-            d = json.load(f)
-        return d
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
     except Exception:
         return None
 
@@ -70,9 +102,10 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.3)  # first sample lands before the timed region ends
         except Exception:
             self.proc = None
         return self
@@ -83,7 +116,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.15)
+            time.sleep(0.1)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -110,71 +143,85 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_rate(threads: int, rows: int, min_seconds: float, seed: int):
-    """Oracle rows/s on `rows` rows of the workload, repeated for >= min_seconds."""
+# ------------------------------------------------------------ CPU oracle ---
+def oracle_rate(rows: int, threads: int, steps: int, min_seconds: float = 0.0, seed: int = SEED):
+    """Oracle rows/s: `steps` passes over `rows` rows (or until min_seconds)."""
     import numpy as np
 
-    import paper_2509_08383_b200 as pam
     from oracle import oracle as orc
-    from paper_2509_08383_b200 import workloads as W
 
-    x = W.gaussian(rows, N_VOCAB, seed=seed)
-    prm = pam.CutMaxParams(p=P_POW, c=C_SCALE, T=T_ITERS).lower()
+    x = gaussian_rows(rows, seed)
+    prm = orc.default_params(T=T_ITERS, p=P_POW, c=C_SCALE)
     done, t0 = 0, time.perf_counter()
-    while True:
-        z, am, st = orc.cutmax_batch(x, prm, nthreads=threads)
+    for i in range(max(1, steps)):
+        _, _, st = orc.cutmax_batch(x, prm, nthreads=threads)
         done += rows
-        el = time.perf_counter() - t0
-        if el >= min_seconds:
+        if min_seconds and time.perf_counter() - t0 >= min_seconds:
             break
-    assert int(np.count_nonzero(st)) == 0
+    el = time.perf_counter() - t0
+    assert int(np.count_nonzero(st & 0xFF)) == 0
     return done / el, done, el
 
 
-def run_reference(args, env):
-    """--impl reference: the CPU oracle with all host threads, same metric/config."""
-    if env.rank != 0:
+def cpu_baseline(all_seconds: float, one_seconds: float) -> dict:
+    """The oracle on this host: all threads (OpenMP over rows) and one thread,
+    each on a bounded sample of the workload's rows."""
+    threads = host_threads()
+    rows_all = max(4 * threads, 64)
+    rate, done, el = oracle_rate(rows_all, threads, steps=1 << 30, min_seconds=all_seconds)
+    rate1, done1, el1 = oracle_rate(8, 1, steps=1 << 30, min_seconds=one_seconds)
+    return {"value": rate, "unit": "rows/s", "cores": threads, "kind": "port",
+            "sample": f"{done} rows x {N_VOCAB} fp64 in {el:.1f} s, OpenMP over rows, {threads} threads",
+            "value_1thread": rate1, "sample_1thread": f"{done1} rows in {el1:.1f} s, 1 thread",
+            "cpu_model": cpu_model()}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on every host thread, the same 4096-row
+    config per step; rank 0 only under torchrun."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     import numpy as np
 
-    import paper_2509_08383_b200 as pam
     from oracle import oracle as orc
-    from paper_2509_08383_b200 import workloads as W
 
-    threads = os.cpu_count() or 1
-    rows = max(threads * 4, 64)
-    x = W.gaussian(rows, N_VOCAB, seed=SEED)
-    prm = pam.CutMaxParams(p=P_POW, c=C_SCALE, T=T_ITERS).lower()
+    threads = host_threads()
+    B = args.rows  # the benched config (4096) unless a test shrinks it
+    x = gaussian_rows(B, SEED)
+    prm = orc.default_params(T=T_ITERS, p=P_POW, c=C_SCALE)
     for _ in range(args.warmup):
-        orc.cutmax_batch(x, prm, nthreads=threads)
-    t0 = time.perf_counter()
+        orc.cutmax_batch(x[:max(threads, 16)], prm, nthreads=threads)  # page-in + thread-pool start
+    times = []
     for _ in range(args.steps):
-        z, am, st = orc.cutmax_batch(x, prm, nthreads=threads)
-    el = time.perf_counter() - t0
-    assert int(np.count_nonzero(st)) == 0
-    rate = rows * args.steps / el
+        t0 = time.perf_counter()
+        _, am, st = orc.cutmax_batch(x, prm, nthreads=threads)
+        times.append(time.perf_counter() - t0)
+    assert int(np.count_nonzero(st & 0xFF)) == 0 and np.array_equal(am, np.argmax(x, axis=1))
+    el = sum(times)
+    rate = B * args.steps / el
     line = {
         "impl": "reference", "metric": "cutmax_rows_per_sec", "value": rate, "unit": "rows/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,3^2) logits, seeded",
-        "config": {"workload": f"C5 B={B_ROWS} x n={N_VOCAB} fp64 T=4 p=3 c=5 (sample of {rows} rows per step)",
-                   "B": B_ROWS, "n": N_VOCAB, "T": T_ITERS, "p": P_POW, "c": C_SCALE},
-        "hbm_gbs": rate * (2 * N_VOCAB * 8 + 4) / 1e9,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic N(0,3^2) logits, seeded (numpy)",
+        "config": {"workload": WORKLOAD, "B": B, "n": N_VOCAB, "T": T_ITERS, "p": P_POW, "c": C_SCALE},
+        "hbm_gbs": rate * BYTES_PER_ROW / 1e9,
         "cpu_baseline": {"value": rate, "unit": "rows/s", "cores": threads, "kind": "port",
-                         "sample": f"{rows} rows x {N_VOCAB} fp64 per step, OpenMP over rows"},
+                         "sample": f"the full {B}-row batch every step, OpenMP over rows", "cpu_model": cpu_model()},
         "e2e": {"value": rate, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_libs": ["oracle/liboracle.so"],
     }
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------- GPU arm ------
 def run_ours(args, env):
     import torch
 
     import paper_2509_08383_b200 as pam
     from paper_2509_08383_b200 import workloads as W
 
-    dev = torch.device("cuda", env.local_rank if env.enabled else 0)
+    dev = torch.device("cuda", env.local_rank % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
     B, n = args.rows, N_VOCAB
     prm = pam.CutMaxParams(p=P_POW, c=C_SCALE, T=T_ITERS)
@@ -190,7 +237,7 @@ def run_ours(args, env):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
-    if int((st != 0).sum()) != 0:
+    if int(((st & 0xFF) != 0).sum()) != 0:
         raise RuntimeError("rows failed in warm-up")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = pam.kernel_launch_count()
@@ -208,12 +255,12 @@ def run_ours(args, env):
     ms = env.max_over_ranks(ms_local)
     total_rows = env.sum_over_ranks(B) * args.steps
     value = total_rows / (ms / 1e3)
-    bytes_per_row = 2 * n * 8 + 4
-    launch_ms = ms_local / args.steps
-    achieved = B * bytes_per_row / (launch_ms / 1e3) / 1e9
+    launch_ms = ms_local / args.steps  # one launch per step, on `stream`
+    achieved = B * BYTES_PER_ROW / (launch_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
-    # parity spot check of the timed output (argmax invariance; rows never fail)
-    ok = bool(torch.equal(am.long(), x.argmax(dim=1))) and int((st != 0).sum()) == 0
+    # argmax invariance over every row of the timed output (rows never fail)
+    ok = bool(torch.equal(am.long(), x.argmax(dim=1))) and int(((st & 0xFF) != 0).sum()) == 0
+    info = pam.launch_info(8, B, n, prm)
 
     # ---- e2e through the host-buffer C ABI (pinned H2D + kernel + D2H) -------
     e2e = None
@@ -246,16 +293,12 @@ def run_ours(args, env):
         e2e_total = env.sum_over_ranks(e2e_rows) * e_steps
         e2e = {"value": e2e_total / el, "unit": "rows/s", "h2d_bytes_per_step": int(e2e_rows * n * 8),
                "d2h_bytes_per_step": int(e2e_rows * (n * 8 + 4 + 4)), "rows_per_step": e2e_rows,
-               "steps": e_steps, "timer": "host wall clock around the synchronous C-ABI call"}
+               "steps": e_steps, "timer": "host wall clock around the synchronous C-ABI call (max over ranks)"}
         ok = ok and bool(torch.equal(ham.long(), x[:e2e_rows].argmax(dim=1).cpu()))
 
     cpu = None
     if env.rank == 0 and env.world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        rate, done, el = cpu_oracle_rate(threads, rows=max(4 * threads, 64), min_seconds=args.cpu_seconds,
-                                         seed=SEED)
-        cpu = {"value": rate, "unit": "rows/s", "cores": threads, "kind": "port",
-               "sample": f"{done} rows x {N_VOCAB} fp64 ({el:.1f} s, OpenMP over rows, all host threads)"}
+        cpu = cpu_baseline(args.cpu_seconds, args.cpu_seconds_1thread)
 
     if env.rank != 0:
         return
@@ -265,21 +308,42 @@ def run_ours(args, env):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic N(0,3^2) logits generated on device from a fixed seed",
-        "config": {"workload": f"C5 B={B} x n={n} fp64, T=4, p=3, c=5 (per GPU)", "B_per_gpu": B, "n": n,
-                   "T": T_ITERS, "p": P_POW, "c": C_SCALE, "invsqrt": "exact",
+        "config": {"workload": WORKLOAD + " (per GPU)", "B_per_gpu": B, "n": n, "T": T_ITERS, "p": P_POW,
+                   "c": C_SCALE, "invsqrt": "exact",
                    "l2": "inputs 4.98 GB per GPU >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"rows sharded, {env.world} independent ranks"},
-        "hbm_gbs": value * bytes_per_row / 1e9,
-        "hbm_frac_of_measured": value * bytes_per_row / 1e9 / peak / env.world,
+                   "parallelism": f"rows sharded, {env.world} independent ranks",
+                   "geometry": f"{info['threads']}x{info['elems_per_thread']} C={info['cluster']}, "
+                               f"{info['clusters']} clusters"},
+        "hbm_gbs": value * BYTES_PER_ROW / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_kind,
-                     "algorithmic_bytes_per_launch": B * bytes_per_row,
+                     "algorithmic_bytes_per_launch": B * BYTES_PER_ROW,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                      "traffic_source": (traffic or {}).get("source")},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "parity_spot_check": ok,
     }
     print(json.dumps(line), flush=True)
+
+
+def run_dry(args, env):
+    """CPU-only check of the multi-rank plumbing (gloo): barrier, max-over-ranks
+    time and whole-job units, no kernels.  Used by tests/test_bench.py."""
+    env.barrier()
+    ms = env.max_over_ranks(1.0 + env.rank)
+    rows = env.sum_over_ranks(args.rows)
+    if env.rank == 0:
+        print(json.dumps({"dry_run": True, "metric": "cutmax_rows_per_sec", "n_gpus": env.world,
+                          "value": rows * args.steps / (ms * args.steps / 1e3), "ms_per_step": ms,
+                          "scaling": "weak"}), flush=True)
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
@@ -292,23 +356,33 @@ def main():
     ap.add_argument("--e2e-rows", type=int, default=B_ROWS)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds-1thread", type=float, default=5.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only (gloo, no GPU work)")
     args = ap.parse_args()
-    args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
-    from paper_2509_08383_b200.dist import init_from_env
+    if args.impl == "ours":
+        args.warmup = max(3, args.warmup)
+
+    # --gpus N outside torchrun: relaunch as N ranks (one process per GPU)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
 
     if args.impl == "reference":
-        # rank 0 alone times the CPU reference; other ranks exit without work
-        from paper_2509_08383_b200.dist import DistEnv
-
-        rank = int(os.environ.get("RANK", "0"))
-        run_reference(args, DistEnv(rank, int(os.environ.get("WORLD_SIZE", "1")), 0, None))
+        run_reference(args)
         return
-    else:
-        env = init_from_env(backend="nccl")
-        run_ours(args, env)
-    env.close()
+    from paper_2509_08383_b200.dist import init_from_env
+
+    env = init_from_env(backend="gloo" if args.dry_run else "nccl")
+    try:
+        if args.dry_run:
+            run_dry(args, env)
+        else:
+            run_ours(args, env)
+    finally:
+        env.close()
 
 
 if __name__ == "__main__":
