@@ -229,9 +229,13 @@ int64_t pam_kernel_launch_count(void);
  *   such variant is compiled.  A forced geometry that cannot hold a row makes the
  *   batch call return PAM_ERR_UNSUPPORTED.
  * pam_set_host_chunk_bytes: pipeline chunk of the host-pointer entry points
- *   (default 128 MiB of input per chunk; <= 0 restores the default). */
+ *   (default 128 MiB of input per chunk; <= 0 restores the default).
+ * pam_set_lean_p3: 1 (default) runs p = 3, T >= 2, aligned fp64 rows on the lean
+ *   kernel (cutmax_p3_kernel.cuh); 0 runs them on the general kernel (A/B tests:
+ *   both give bit-identical results). */
 int pam_set_geometry_override(int dtype_bytes, int threads, int elems_per_thread, int cluster, int min_blocks);
 int pam_set_host_chunk_bytes(int64_t bytes);
+int pam_set_lean_p3(int on);
 /* Debug: device buffer (grid x 8 rows x 32 events of int64 clock64 stamps) that
  * the CutMax kernel fills with per-CTA phase timestamps; NULL disables. */
 void pam_set_trace_buffer(long long* d_buf, int64_t entries);

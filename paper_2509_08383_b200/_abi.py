@@ -103,6 +103,7 @@ SIGNATURES = {
     "pam_last_cuda_error": (C.c_char_p, []),
     "pam_set_trace_buffer": (None, [_P, _I64]),
     "pam_set_geometry_override": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "pam_set_lean_p3": (C.c_int, [C.c_int]),
     "pam_set_host_chunk_bytes": (C.c_int, [_I64]),
     "pam_convergence_trace_batch_f64": (C.c_int, [_P, _I64, _I64, _I64, C.POINTER(pam_cutmax_params), _P, _P, _P]),
     "pam_cutmax_jvp_batch_f64": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(pam_cutmax_params), _P, _P, _I64,

@@ -108,6 +108,15 @@ struct __align__(16) ControlBlock {
   double2 tin[2][16];    // input top-2 records (TieWarning) per cluster rank, by local row parity
   double2 wt2[32];       // per-warp top-2 partials
   unsigned long long mb_t[2];
+  long long unc_rows[16];  // rows whose TieWarning the key screen left undecided (settled at kernel end)
+  int unc_n;               // their count (> 16: re-scan every row of the cluster)
+  // control warp: a finished row whose argmax / status is written in the next
+  // row's first exchange wait (kept here, not in registers)
+  long long fin_row, fin_best;
+  int fin_st, fin_pending;
+  // control warp's scalar state of the lean p = 3 kernel (cutmax_p3_kernel.cuh)
+  double p3_S, p3_Q, p3_R, p3_dm, p3_s2, p3_m3, p3_e1, p3_w;
+  int p3_st;
   unsigned long long mb_load;
   unsigned long long mb_x[2];
   unsigned long long mb_g;
@@ -237,6 +246,107 @@ __device__ __forceinline__ void bfly_top2(double& a1, double& a2) {
 __device__ __forceinline__ int tie_flag(int st, double2 t) {
   return (st == PAM_OK && t.x - t.y < 1e-9) ? PAM_ROW_FLAG_TIE : 0;
 }
+
+// ---------------------------------------------------------------------------
+// Input top-2 screen of the rows kernel (TieWarning).  Each
+// thread keeps the top-2 of a 32-bit image of its inputs -- the high word of a
+// double (sign, exponent, 20 mantissa bits), or a whole float -- on the FP32
+// pipe (hiword_f below) instead of three fp64 min/max per element on the DP
+// pipe the passes saturate; warps combine signed order keys of those images
+// (fkey) with REDUX.  For fp32 rows the image is exact; for fp64 each key
+// brackets its value, and tie_decide() turns the cluster's top-2 keys
+// (K1 >= K2) into a certain flag or "undecided" (the brackets straddle the
+// 1e-9 threshold, e.g. a duplicated maximum), which the kernel settles with an
+// exact fp64 re-scan of the row at its end.
+__device__ __forceinline__ void top2k_add(int& k1, int& k2, int k) {
+  k2 = max(k2, min(k1, k));
+  k1 = max(k1, k);
+}
+// The per-element screen runs on the FP32 pipe: the high word of a double,
+// read as an fp32 bit pattern (sign, 8 of the 11 exponent bits, ...), orders
+// exactly like the double's high word (sign-magnitude both ways).  Patterns
+// that read as fp32 Inf / NaN need |x| >= 2^1017, where the row's variance
+// overflows (status RANGE, no TieWarning).  fp32 rows use the value itself.
+__device__ __forceinline__ float hiword_f(double x) { return __int_as_float(__double2hiint(x)); }
+__device__ __forceinline__ float hiword_f(float x) { return x; }
+__device__ __forceinline__ void top2f_add(float& m1, float& m2, float x) {
+  m2 = fmaxf(m2, fminf(m1, x));
+  m1 = fmaxf(m1, x);
+}
+// order key of a screen value (int order = value order; -inf -> a finite key)
+__device__ __forceinline__ int fkey(float f) {
+  const int h = __float_as_int(f);
+  return h ^ ((h >> 31) & 0x7fffffff);
+}
+// Multiset top-2 of the lanes' (k1 >= k2) pairs; every lane gets the result.
+// Lanes without data must hold INT_MIN (the key of no finite value).
+__device__ __forceinline__ void top2k_warp(int& k1, int& k2) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int m1 = __reduce_max_sync(FULL, k1);
+  const unsigned dup = __ballot_sync(FULL, k1 == m1);
+  const int m2 = __reduce_max_sync(FULL, k1 == m1 ? k2 : k1);
+  k2 = __popc(dup) > 1 ? m1 : m2;
+  k1 = m1;
+}
+__device__ __forceinline__ unsigned long long pack_keys(int k1, int k2) {
+  return ((unsigned long long)(unsigned)k1 << 32) | (unsigned)k2;
+}
+__device__ __forceinline__ int2 unpack_keys(unsigned long long u) {
+  return make_int2((int)(unsigned)(u >> 32), (int)(unsigned)u);
+}
+// Bracket [lo, hi] of the values whose key is k (fp64 high-word keys).
+__device__ __forceinline__ void key_bracket(int k, double& lo, double& hi) {
+  const int h = k ^ ((k >> 31) & 0x7fffffff);  // the map is an involution
+  const double a = __hiloint2double(h, 0), b = __hiloint2double(h, (int)0xffffffff);
+  lo = fmin(a, b);
+  hi = fmax(a, b);
+}
+// 0: no tie, 1: tie (oracle: m1 - m2 < 1e-9), 2: undecided (fp64 only).
+// fl() is monotone, so a bound on the exact gap bounds the oracle's rounded one.
+template <typename Elem>
+__device__ __forceinline__ int tie_decide(int st, int K1, int K2) {
+  if (st != PAM_OK) return 0;
+  if (sizeof(Elem) == 4) {  // exact keys: the float values themselves
+    const int h1 = K1 ^ ((K1 >> 31) & 0x7fffffff), h2 = K2 ^ ((K2 >> 31) & 0x7fffffff);
+    return ((double)__int_as_float(h1) - (double)__int_as_float(h2) < 1e-9) ? 1 : 0;
+  }
+  double l1, h1, l2, h2;
+  key_bracket(K1, l1, h1);
+  key_bracket(K2, l2, h2);
+  if (l1 - h2 >= 1e-9) return 0;
+  if (h1 - l2 < 1e-9) return 1;
+  return 2;
+}
+// The same decision from the keys of the SHIFTED input v = fl(x - K0) (the
+// lean p = 3 kernel screens its first pass, where v is in registers).  v is a
+// monotone function of x, so the top-2 of v are the images of the top-2 of x,
+// and x1 - x2 = (v1 - v2) + (e1 - e2) with |e_i| <= ulp(v_i) / 2 (fp32 rows:
+// fp32 ulps).  The slack below covers those and the rounding of this bound.
+template <typename Elem>
+__device__ __forceinline__ int tie_decide_shifted(int st, int K1, int K2) {
+  if (st != PAM_OK) return 0;
+  double l1, h1, l2, h2;
+  if (sizeof(Elem) == 4) {
+    const int a1 = K1 ^ ((K1 >> 31) & 0x7fffffff), a2 = K2 ^ ((K2 >> 31) & 0x7fffffff);
+    l1 = h1 = (double)__int_as_float(a1);
+    l2 = h2 = (double)__int_as_float(a2);
+  } else {
+    key_bracket(K1, l1, h1);
+    key_bracket(K2, l2, h2);
+  }
+  const double rel = sizeof(Elem) == 4 ? 0x1p-22 : 0x1p-50;
+  const double slack = (fabs(l1) + fabs(h1) + fabs(l2) + fabs(h2)) * rel + 0x1p-1000;
+  if ((l1 - h2) - slack >= 1e-9) return 0;
+  if ((h1 - l2) + slack < 1e-9) return 1;
+  return 2;
+}
+
+struct KeyPush {
+  bool on;
+  int k1, k2;
+  uint32_t slot;
+  bool stashed = false;  // the warps already stashed their records (wt2): only the CTA combine + send remain
+};
 // Top-2 side record of an exchange: the CTA's pair, butterflied over each
 // warp, goes to slot `slot` (the row's local parity) of every CTA with its own
 // mbarrier mb_t[slot]; top2_wait (warp 0, at the row's status write) combines
@@ -264,6 +374,68 @@ __device__ __forceinline__ double2 top2_wait(ControlBlock* cb, const uint32_t sl
   return make_double2(m1, m2);
 }
 
+// Row lr's input top-2 keys: slot lr & 1, the (lr >> 1)-th phase of that slot's
+// mbarrier (stateless, so any warp can wait; lane 0 of the caller re-arms).
+__device__ __forceinline__ int2 top2k_wait_row(ControlBlock* cb, const int64_t lr, const uint32_t C, const int lane) {
+  const uint32_t slot = (uint32_t)(lr & 1);
+  ptx::mbar_wait_cta(ptx::smem_addr(&cb->mb_t[slot]), (uint32_t)((lr >> 1) & 1));
+  const bool have = lane < (int)C;
+  const int2 rec = unpack_keys((unsigned long long)__double_as_longlong(cb->tin[slot][have ? lane : 0].x));
+  __syncwarp();
+  if (lane == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[slot]), C * 16u);  // arm row + 2
+  int k1 = have ? rec.x : INT_MIN, k2 = have ? rec.y : INT_MIN;
+  top2k_warp(k1, k2);
+  return make_int2(k1, k2);
+}
+__device__ __forceinline__ int2 top2k_wait(ControlBlock* cb, const uint32_t slot, uint32_t& phases, const uint32_t C,
+                                           const int gtid) {
+  const int lane = gtid & 31;
+  ptx::mbar_wait_cta(ptx::smem_addr(&cb->mb_t[slot]), (phases >> slot) & 1u);
+  phases ^= 1u << slot;
+  const bool have = lane < (int)C;
+  const int2 rec = unpack_keys((unsigned long long)__double_as_longlong(cb->tin[slot][have ? lane : 0].x));
+  __syncwarp();
+  if (gtid == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[slot]), C * 16u);  // arm row + 2
+  int k1 = have ? rec.x : INT_MIN, k2 = have ? rec.y : INT_MIN;
+  top2k_warp(k1, k2);
+  return make_int2(k1, k2);
+}
+
+// Per-warp stash and CTA-level push of a top-2 side record: exact fp64 pairs
+// (Top2Push, sampler) or order keys (KeyPush, rows kernel).
+__device__ __forceinline__ bool t2_stashed(const Top2Push&) { return false; }
+__device__ __forceinline__ bool t2_stashed(const KeyPush& t) { return t.stashed; }
+__device__ __forceinline__ void t2_warp(Top2Push& t) { bfly_top2<32>(t.m1, t.m2); }
+__device__ __forceinline__ void t2_warp(KeyPush& t) { top2k_warp(t.k1, t.k2); }
+__device__ __forceinline__ void t2_stash(ControlBlock* cb, int warp, const Top2Push& t) {
+  cb->wt2[warp] = make_double2(t.m1, t.m2);
+}
+__device__ __forceinline__ void t2_stash(ControlBlock* cb, int warp, const KeyPush& t) {
+  cb->wt2[warp] = make_double2(__longlong_as_double((long long)pack_keys(t.k1, t.k2)), 0.0);
+}
+template <int NW>
+__device__ __forceinline__ void t2_send(ControlBlock* cb, int lane, uint32_t rank, uint32_t C, const Top2Push& t) {
+  const double2 w2 = cb->wt2[lane & (NW - 1)];
+  double m1 = w2.x, m2 = w2.y;
+  bfly_top2<NW>(m1, m2);
+  if (lane < (int)C)
+    ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->tin[t.slot][rank]), (uint32_t)lane), m1, m2,
+                        ptx::mapa(ptx::smem_addr(&cb->mb_t[t.slot]), (uint32_t)lane));
+}
+template <int NW>
+__device__ __forceinline__ void t2_send(ControlBlock* cb, int lane, uint32_t rank, uint32_t C, const KeyPush& t) {
+  int k1 = INT_MIN, k2 = INT_MIN;
+  if (lane < NW) {
+    const int2 r = unpack_keys((unsigned long long)__double_as_longlong(cb->wt2[lane].x));
+    k1 = r.x;
+    k2 = r.y;
+  }
+  top2k_warp(k1, k2);
+  if (lane < (int)C)
+    ptx::st_async_b64x2(ptx::mapa(ptx::smem_addr(&cb->tin[t.slot][rank]), (uint32_t)lane), pack_keys(k1, k2), 0ull,
+                        ptx::mapa(ptx::smem_addr(&cb->mb_t[t.slot]), (uint32_t)lane));
+}
+
 // ---------------------------------------------------------------------------
 // Cluster exchange, split in two so independent work can run between the push
 // and the wait.  All NTG threads of the CTA call both halves.
@@ -279,32 +451,38 @@ struct NoSide {
 
 // Exchange payloads: two sums; three sums (the third rides in the candidate
 // slot); or two sums plus the lexicographic (value desc, index asc) argmax.
-enum XchMode { kSum2 = 0, kSum3 = 1, kArgmax = 2 };
+enum XchMode { kSum2 = 0, kSum3 = 1, kArgmax = 2, kTop2 = 3 };  // kTop2: (a, b) = exact top-2 pair
 
 // kSum3 with third == false behaves as kSum2 (one code copy for both in the p = 3 row loop).
-template <int NTG, int MODE, typename Ch, typename Side = NoSide>
+template <int NTG, int MODE, typename Ch, typename Side = NoSide, typename T2 = Top2Push>
 __device__ __forceinline__ void xch_push(double a, double b, double c, long long ci_, Ch* cb,
                                          const uint32_t round, const uint32_t rank, const uint32_t C, const int gtid,
                                          const Side& side = Side(), const bool third = true,
-                                         Top2Push t2 = no_top2()) {
+                                         T2 t2 = T2{false}) {
   constexpr int NW = NTG / 32;
   const int lane = gtid & 31, warp = gtid >> 5;
   long long ci = ci_;
-  bfly_sum2<32>(a, b);
+  if (MODE == kTop2)
+    bfly_top2<32>(a, b);
+  else
+    bfly_sum2<32>(a, b);
   if (MODE == kArgmax) bfly_argmax<32>(c, ci);
   if (MODE == kSum3 && third) bfly_sum1<32>(c);
-  if (t2.on) bfly_top2<32>(t2.m1, t2.m2);
+  if (t2.on && !t2_stashed(t2)) t2_warp(t2);
   if (lane == 0) {
     cb->wred[warp] = make_double2(a, b);
     if (MODE == kArgmax || (MODE == kSum3 && third)) cb->wcand[warp] = make_double2(c, __longlong_as_double(ci));
-    if (t2.on) cb->wt2[warp] = make_double2(t2.m1, t2.m2);
+    if (t2.on && !t2_stashed(t2)) t2_stash(cb, warp, t2);
   }
   __syncthreads();
   const uint32_t par = round & 1u;
   if (warp == 0) {
     const double2 w = cb->wred[lane & (NW - 1)];
     double ca = w.x, cbv = w.y;
-    bfly_sum2<NW>(ca, cbv);
+    if (MODE == kTop2)
+      bfly_top2<NW>(ca, cbv);
+    else
+      bfly_sum2<NW>(ca, cbv);
     double cv = -HUGE_VAL;
     long long cix = 0x7fffffffffffffffLL;
     if (MODE == kArgmax || (MODE == kSum3 && third)) {
@@ -320,14 +498,7 @@ __device__ __forceinline__ void xch_push(double a, double b, double c, long long
       ptx::st_async_b64x2(ptx::mapa(ptx::smem_addr(&cb->xch[par][rank].cand), (uint32_t)lane),
                           (uint64_t)__double_as_longlong(cv), (uint64_t)cix, bar);
     }
-    if (t2.on) {
-      const double2 w2 = cb->wt2[lane & (NW - 1)];
-      double m1 = w2.x, m2 = w2.y;
-      bfly_top2<NW>(m1, m2);
-      if (lane < (int)C)
-        ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->tin[t2.slot][rank]), (uint32_t)lane), m1, m2,
-                            ptx::mapa(ptx::smem_addr(&cb->mb_t[t2.slot]), (uint32_t)lane));
-    }
+    if (t2.on) t2_send<NW>(cb, lane, rank, C, t2);
   } else if (warp == NW - 1 && lane == 0) {
     side();
   }
@@ -346,9 +517,12 @@ __device__ __forceinline__ double2 xch_wait(double& c, long long& ci, Ch* cb, ui
   const int src = lane & 15;
   const bool have = src < (int)C;
   const XchRecord rec = cb->xch[par][have ? src : 0];
-  double a = have ? rec.ab.x : 0.0;
-  double b = have ? rec.ab.y : 0.0;
-  bfly_sum2<16>(a, b);
+  double a = have ? rec.ab.x : (MODE == kTop2 ? -HUGE_VAL : 0.0);
+  double b = have ? rec.ab.y : (MODE == kTop2 ? -HUGE_VAL : 0.0);
+  if (MODE == kTop2)
+    bfly_top2<16>(a, b);
+  else
+    bfly_sum2<16>(a, b);
   if (MODE == kArgmax) {
     c = have ? rec.cand.x : -HUGE_VAL;
     ci = have ? __double_as_longlong(rec.cand.y) : 0x7fffffffffffffffLL;
@@ -362,62 +536,68 @@ __device__ __forceinline__ double2 xch_wait(double& c, long long& ci, Ch* cb, ui
   return make_double2(a, b);
 }
 
-template <int NTG, bool ARGMAX, typename Ch>
+template <int NTG, bool ARGMAX, typename Ch, typename T2 = Top2Push>
 __device__ __forceinline__ double2 cluster_reduce(double a, double b, double& best, long long& besti, Ch* cb,
                                                   uint32_t& round, const uint32_t rank, const uint32_t C,
-                                                  const int gtid, Top2Push t2 = no_top2()) {
+                                                  const int gtid, T2 t2 = T2{false}) {
   constexpr int M = ARGMAX ? kArgmax : kSum2;
   xch_push<NTG, M>(a, b, best, besti, cb, round, rank, C, gtid, NoSide(), true, t2);
   return xch_wait<M>(best, besti, cb, round, C, gtid);
 }
 
-template <int NTG, typename Ch>
+template <int NTG, typename Ch, typename T2 = Top2Push>
 __device__ __forceinline__ double2 cluster_sum2(double a, double b, Ch* cb, uint32_t& round,
                                                 const uint32_t rank, const uint32_t C, const int gtid,
-                                                Top2Push t2 = no_top2()) {
+                                                T2 t2 = T2{false}) {
   double bv = 0.0;
   long long bi = 0;
   return cluster_reduce<NTG, false>(a, b, bv, bi, cb, round, rank, C, gtid, t2);
 }
 
 // Three cluster sums in one exchange.
-template <int NTG, typename Ch>
+template <int NTG, typename Ch, typename T2 = Top2Push>
 __device__ __forceinline__ double3 cluster_sum3(double a, double b, double c, Ch* cb, uint32_t& round,
                                                 const uint32_t rank, const uint32_t C, const int gtid,
-                                                Top2Push t2 = no_top2()) {
+                                                T2 t2 = T2{false}) {
   long long ci = 0;
   xch_push<NTG, kSum3>(a, b, c, ci, cb, round, rank, C, gtid, NoSide(), true, t2);
   const double2 r = xch_wait<kSum3>(c, ci, cb, round, C, gtid);
   return make_double3(r.x, r.y, c);
 }
 
+// Exact top-2 of (m1, m2) pairs over the cluster (every thread calls it).
+template <int NTG, typename Ch>
+__device__ __forceinline__ double2 cluster_top2(double m1, double m2, Ch* cb, uint32_t& round, const uint32_t rank,
+                                                const uint32_t C, const int gtid) {
+  double c = 0.0;
+  long long ci = 0;
+  xch_push<NTG, kTop2>(m1, m2, c, ci, cb, round, rank, C, gtid);
+  return xch_wait<kTop2>(c, ci, cb, round, C, gtid);
+}
+
 // Next row's input sums (row-boundary exchange, second record): own per-warp
 // slots, own records and mbarrier (mb_in, one phase per row).
 template <int NTG>
 __device__ __forceinline__ void xin_push(double s, double q, ControlBlock* cb, const uint32_t rank, const uint32_t C,
-                                         const int gtid, Top2Push t2) {
+                                         const int gtid, KeyPush t2) {
   constexpr int NW = NTG / 32;
   const int lane = gtid & 31, warp = gtid >> 5;
   bfly_sum2<32>(s, q);
-  bfly_top2<32>(t2.m1, t2.m2);
+  t2_warp(t2);
   if (lane == 0) {
     cb->wred2[warp] = make_double2(s, q);
-    cb->wt2[warp] = make_double2(t2.m1, t2.m2);
+    t2_stash(cb, warp, t2);
   }
   __syncthreads();
   if (warp == 0) {
     const double2 w = cb->wred2[lane & (NW - 1)];
     double cs = w.x, cq = w.y;
     bfly_sum2<NW>(cs, cq);
-    const double2 w2 = cb->wt2[lane & (NW - 1)];
-    double m1 = w2.x, m2 = w2.y;
-    bfly_top2<NW>(m1, m2);
     if (lane < (int)C) {
       const uint32_t bar = ptx::mapa(ptx::smem_addr(&cb->mb_in), (uint32_t)lane);
       ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->xin[rank]), (uint32_t)lane), cs, cq, bar);
-      ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->tin[t2.slot][rank]), (uint32_t)lane), m1, m2,
-                          ptx::mapa(ptx::smem_addr(&cb->mb_t[t2.slot]), (uint32_t)lane));
     }
+    t2_send<NW>(cb, lane, rank, C, t2);
   }
 }
 
@@ -865,6 +1045,8 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
   if (TMA) policy = ptx::policy_evict_first();
 
   if (gtid == 0) {
+    cb->unc_n = 0;
+    cb->fin_pending = 0;
     ptx::mbar_init(bar_load, 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[0]), 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[1]), 1);
@@ -912,9 +1094,9 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
   uint32_t t2_ph = 0u;           // mb_t phases, bit s = slot s (warp 0)
   int64_t lrow = 0;              // local row counter: the parity selects the top-2 record slot
   Elem v[E];
-  // top-2 of the real input elements of this thread's slots (TieWarning);
-  // phantom slots are copies of x[0] and must not count as a second maximum
-  Elem t1 = -INFINITY, t2 = -INFINITY;
+  // top-2 screen values (hiword_f) of the real input elements of this thread's
+  // slots (TieWarning); phantom slots are copies of x[0] and must not count
+  float t1 = -INFINITY, t2 = -INFINITY;
   auto load_direct = [&](const Elem* src, Elem k0e) {  // unaligned rows: direct loads, no staging
 #pragma unroll
     for (int kk = 0; kk < NV; ++kk) {
@@ -924,8 +1106,25 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         const bool in = li0 + j < len;
         const Elem xv = in ? __ldcs(src + li0 + j) : k0e;
         v[kk * VEC + j] = xv;
-        if (in) top2_add(t1, t2, xv);
+        if (in) top2f_add(t1, t2, hiword_f(xv));
       }
+    }
+  };
+
+  // warp 0, once per row: the row's input top-2 keys -> TieWarning decision;
+  // rank 0 writes argmax and status, undecided rows are queued (every CTA
+  // queues identically: the keys are cluster-uniform)
+  auto finish_row = [&](int64_t r, int st, long long amax, uint32_t slot) {
+    const int2 kk = top2k_wait(cb, slot, t2_ph, C, gtid);
+    const int td = tie_decide<Elem>(st, kk.x, kk.y);
+    if (rank == 0 && gtid == 0) {
+      if (a.argmax) a.argmax[r] = (st == PAM_OK) ? (int32_t)amax : -1;
+      if (a.status) a.status[r] = st | (td == 1 ? PAM_ROW_FLAG_TIE : 0);
+    }
+    if (td == 2 && gtid == 0) {
+      const int q = cb->unc_n;
+      if (q < 16) cb->unc_rows[q] = r;
+      cb->unc_n = q + 1;
     }
   };
 
@@ -944,13 +1143,13 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       if (li0 + VEC <= len) {
         *reinterpret_cast<V*>(&v[k * VEC]) = *reinterpret_cast<const V*>(buf + li0);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) top2_add(t1, t2, v[k * VEC + j]);
+        for (int j = 0; j < VEC; ++j) top2f_add(t1, t2, hiword_f(v[k * VEC + j]));
       } else {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
           const bool in = li0 + j < len;
           v[k * VEC + j] = in ? buf[li0 + j] : k0;  // phantoms = K0
-          if (in) top2_add(t1, t2, v[k * VEC + j]);
+          if (in) top2f_add(t1, t2, hiword_f(v[k * VEC + j]));
         }
       }
     }
@@ -1009,7 +1208,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         }
         const double3 part = input_pass3<Elem, E>(v, K0);
         const double3 r = cluster_sum3<NTG>(part.x, part.y, part.z, cb, xround, rank, C, gtid,
-                                            Top2Push{true, (double)t1, (double)t2, (uint32_t)(lrow & 1)});
+                                            KeyPush{true, fkey(t1), fkey(t2), (uint32_t)(lrow & 1)});
         S_c = r.x;
         Q_c = r.y;
         R_c = r.z;
@@ -1244,6 +1443,11 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
           xch_push<NTG, kSum2>(part.x, part.y, 0.0, 0LL, cb, xround, rank, C, gtid, [&]() { side(t); });
         PAM_TRACE(tr, 16 + t);
         if (warp == 0) {
+          if (t == 0 && cb->fin_pending) {  // previous row's argmax / status, in the exchange's idle window
+            finish_row(cb->fin_row, cb->fin_st, cb->fin_best, (uint32_t)((lrow - 1) & 1));
+            __syncwarp();
+            if (gtid == 0) cb->fin_pending = 0;
+          }
           double r3 = 0.0;
           long long ci = 0;
           const double2 r = need3 ? xch_wait<kSum3>(r3, ci, cb, xround, C, gtid)
@@ -1335,7 +1539,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
 #pragma unroll
               for (int j = 0; j < VEC; ++j) {
                 v[kk * VEC + j] = xe[j] - k0next;
-                top2_add(t1, t2, xe[j]);
+                top2f_add(t1, t2, hiword_f(xe[j]));
               }
             }
           } else {
@@ -1345,7 +1549,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
               Elem xv = k0next;  // phantoms: K0(next) -> 0
               if (MODE == 0 && in) {
                 xv = buf[li0 + j];
-                top2_add(t1, t2, xv);
+                top2f_add(t1, t2, hiword_f(xv));
               }
               if (in) buf[li0 + j] = o[j];
               if (MODE == 0) v[kk * VEC + j] = xv - k0next;
@@ -1388,8 +1592,9 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       long long besti = base + (long long)(((besto / VEC) * NTG + gtid) * VEC + (besto % VEC));
       const int64_t zr = row;
       xch_push<NTG, kArgmax>(
-          nxt.x, nxt.y, best, besti, cb, xround, rank, C, gtid, [&]() { if (TMA) store_all(zr); }, true,
-          Top2Push{merged, (double)t1, (double)t2, (uint32_t)((lrow + 1) & 1)});
+          nxt.x, nxt.y, best, besti, cb, xround, rank, C, gtid,
+          [&]() { if (TMA) store_all(zr); }, true,
+          KeyPush{merged, fkey(t1), fkey(t2), (uint32_t)((lrow + 1) & 1)});
       if (merged && T == 1) {
         // T = 1 needs the next input's third power sum too (one more exchange)
         if (warp == 0) {
@@ -1411,11 +1616,17 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       PAM_TRACE(tr, 6 + 2 * (T - 1));
       in_ready = merged;
       k0_cur = k0next;
-      if (warp == 0) {  // this row's input top-2 arrived long ago (input / previous closing exchange)
-        const double2 tt = top2_wait(cb, (uint32_t)(lrow & 1), t2_ph, C, gtid);
-        if (rank == 0 && gtid == 0) {
-          if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)besti : -1;
-          if (a.status) a.status[row] = st | tie_flag(st, tt);
+      if (warp == 0) {
+        // argmax / status / TieWarning of this row: deferred to the next row's
+        // first exchange wait (the input top-2 records arrived long ago, but the
+        // wait and the decision would sit on the control warp's critical path)
+        if (T == 1 || !merged) {
+          finish_row(row, st, besti, (uint32_t)(lrow & 1));
+        } else if (gtid == 0) {
+          cb->fin_row = row;
+          cb->fin_st = st;
+          cb->fin_best = besti;
+          cb->fin_pending = 1;
         }
       }
       PAM_TRACE(tr, 21);
@@ -1454,7 +1665,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         }
         const double2 part = input_pass<Elem, E>(v, K0);
         const double2 r = cluster_sum2<NTG>(part.x, part.y, cb, xround, rank, C, gtid,
-                                            Top2Push{true, (double)t1, (double)t2, (uint32_t)(lrow & 1)});
+                                            KeyPush{true, fkey(t1), fkey(t2), (uint32_t)(lrow & 1)});
         S_in = r.x;
         Q_in = r.y;
       }
@@ -1503,7 +1714,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
   #pragma unroll
               for (int j = 0; j < VEC; ++j) {
                 v[kk * VEC + j] = xe[j] - k0next;
-                top2_add(t1, t2, xe[j]);
+                top2f_add(t1, t2, hiword_f(xe[j]));
               }
             } else {
   #pragma unroll
@@ -1512,7 +1723,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
                 const Elem xv = in ? buf[li0 + j] : k0next;  // phantoms: K0(next) -> 0
                 if (in) {
                   buf[li0 + j] = v[kk * VEC + j];
-                  top2_add(t1, t2, xv);
+                  top2f_add(t1, t2, hiword_f(xv));
                 }
                 v[kk * VEC + j] = xv - k0next;
               }
@@ -1527,7 +1738,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
             }
           }
           xin_push<NTG>((double)sa + (double)sb, (double)qa + (double)qb, cb, rank, C, gtid,
-                        Top2Push{true, (double)t1, (double)t2, (uint32_t)((lrow + 1) & 1)});
+                        KeyPush{true, fkey(t1), fkey(t2), (uint32_t)((lrow + 1) & 1)});
           PAM_TRACE(tr, 24);
         }
         double2 r = xch_wait<kArgmax>(best, besti, cb, xround, C, gtid);
@@ -1546,13 +1757,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
           v, S_in, Q_in, K0, len, mph, rp, a.inv_n, (double)n, cb, xround, rank, C, gtid, base,
           (rank == 0 && gtid == 0 && a.stats) ? a.stats + row * T * 2 : nullptr, rnorm, amax, hooks, tr);
       PAM_TRACE(tr, 20);
-      if (warp == 0) {
-        const double2 tt = top2_wait(cb, (uint32_t)(lrow & 1), t2_ph, C, gtid);
-        if (rank == 0 && gtid == 0) {
-          if (a.argmax) a.argmax[row] = (st == PAM_OK) ? (int32_t)amax : -1;
-          if (a.status) a.status[row] = st | tie_flag(st, tt);
-        }
-      }
+      if (warp == 0) finish_row(row, st, amax, (uint32_t)(lrow & 1));
 
       const Elem re = (Elem)rnorm;
       if (merged) {
@@ -1597,6 +1802,25 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       }
       k0_cur = k0next;
       PAM_TRACE(tr, 21);
+    }
+  }
+  // ---- TieWarning rows the key screen left undecided: exact fp64 top-2 -------
+  // (rare: the two largest inputs share their high word, e.g. a duplicated
+  // maximum).  The queue is identical in every CTA of the cluster.
+  __syncthreads();
+  const int unc = cb->unc_n;
+  if (unc > 0 && a.status) {
+    const int64_t cnt = unc <= 16 ? unc : (a.B - cid + ncl - 1) / ncl;  // overflow: every row of the cluster
+    for (int64_t j = 0; j < cnt; ++j) {
+      const int64_t r = unc <= 16 ? cb->unc_rows[j] : cid + j * ncl;
+      const Elem* xr = X + r * a.ldx + base;
+      double m1 = -HUGE_VAL, m2 = -HUGE_VAL;
+      for (int i = gtid; i < len; i += NTG) top2_add(m1, m2, (double)xr[i]);
+      const double2 t = cluster_top2<NTG>(m1, m2, cb, xround, rank, C, gtid);
+      if (rank == 0 && gtid == 0) {
+        const int s0 = a.status[r];
+        if ((s0 & 0xff) == PAM_OK) a.status[r] = (s0 & ~PAM_ROW_FLAG_TIE) | (t.x - t.y < 1e-9 ? PAM_ROW_FLAG_TIE : 0);
+      }
     }
   }
   if (TMA && dma) ptx::bulk_wait_all();  // Z stores complete before the CTA retires

@@ -12,6 +12,9 @@ namespace pam {
           (const void*)cutmax_rows_kernel<double, NTG, E, 3, MINB>, STOPFN                                  \
     }                                                                                                       \
   }
+// p = 3 only (the generic flow does not fit these register budgets)
+#define PAM_W(NTG, E, MINB) \
+  { 8, NTG, E, MINB, {nullptr, (const void*)cutmax_rows_kernel<double, NTG, E, 3, MINB>, nullptr} }
 #define PAM_STOP(NTG, E, MINB) (const void*)cutmax_rows_kernel<double, NTG, E, 0, MINB, true>
 
 const Variant kCutmaxVariantsF64[] = {

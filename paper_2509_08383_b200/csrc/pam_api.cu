@@ -40,6 +40,7 @@ struct Overrides {
   std::atomic<int> ntg[2]{{0}, {0}}, e[2]{{0}, {0}}, c[2]{{0}, {0}}, minb[2]{{0}, {0}};  // [fp32, fp64]
   std::atomic<int64_t> host_chunk_bytes{128ll << 20};
   std::atomic<int> generation{0};  // bumped on every override change: invalidates the geometry cache
+  std::atomic<int> lean{1};        // 0: p = 3 rows always run the general kernel (pam_set_lean_p3, A/B tests)
 };
 Overrides g_ovr;
 
@@ -280,6 +281,13 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   const Geometry g = choose_geometry((int)sizeof(Elem), B, n, flavour);
   if (!g.var) return PAM_ERR_UNSUPPORTED;
   const void* fn = g.var->fn[flavour];
+  // p = 3 everywhere, T >= 2, aligned rows: the lean kernel of the same geometry
+  if (flavour == 1 && tma && prm->T >= 2 && sizeof(Elem) == 8 && g_ovr.lean.load()) {
+    for (int i = 0; i < kNumCutmaxP3F64; ++i) {
+      const LeanVariant& lv = kCutmaxP3F64[i];
+      if (lv.ntg == g.var->ntg && lv.e == g.var->e && lv.minb == g.var->minb) fn = lv.fn;
+    }
+  }
   // the row buffer is sized for the full capacity even without TMA so the
   // occupancy (and the chooser's estimate) does not depend on alignment
   const int smem = smem_bytes(*g.var);
@@ -697,6 +705,10 @@ int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_par
   info->groups = 1;
   const VariantTable& tab = kCutmaxTables[dtype_bytes == 8 ? 1 : 0];
   info->kernel_id = (int)(g.var - tab.v) + 100 * flavour;
+  if (flavour == 1 && dtype_bytes == 8 && prm->T >= 2 && g_ovr.lean.load())
+    for (int i = 0; i < kNumCutmaxP3F64; ++i)
+      if (kCutmaxP3F64[i].ntg == g.var->ntg && kCutmaxP3F64[i].e == g.var->e && kCutmaxP3F64[i].minb == g.var->minb)
+        info->kernel_id += 1000;  // lean p = 3 kernel (aligned rows)
   return PAM_OK;
 }
 
@@ -716,6 +728,11 @@ int pam_set_geometry_override(int dtype_bytes, int threads, int elems_per_thread
   g_ovr.c[oi] = cluster;
   g_ovr.minb[oi] = min_blocks;
   g_ovr.generation.fetch_add(1);
+  return PAM_OK;
+}
+
+int pam_set_lean_p3(int on) {
+  g_ovr.lean = on ? 1 : 0;
   return PAM_OK;
 }
 

@@ -33,6 +33,15 @@ struct SamplerVariant {
   const void* stop[2];   // generic p with early stopping, [GUMBEL]
 };
 
+// Lean p = 3 kernels (cutmax_p3_kernel.cuh), matched to a Variant by
+// (elem_bytes, ntg, e, minb).
+struct LeanVariant {
+  int elem_bytes, ntg, e, minb;
+  const void* fn;
+};
+extern const LeanVariant kCutmaxP3F64[];
+extern const int kNumCutmaxP3F64;
+
 extern const Variant kCutmaxVariantsF64[];
 extern const int kNumCutmaxVariantsF64;
 extern const Variant kCutmaxVariantsF32[];

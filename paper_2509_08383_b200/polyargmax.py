@@ -605,3 +605,17 @@ class geometry_override:
     def __exit__(self, *exc):
         _lib.pam_set_geometry_override(self.args[0], 0, 0, 0, 0)
         return False
+
+
+class general_p3_kernel:
+    """Test hook: inside the ``with`` block, p = 3 rows run on the general
+    CutMax kernel instead of the lean p = 3 kernel (pam_set_lean_p3(0)); both
+    must give bit-identical results."""
+
+    def __enter__(self):
+        _lib.pam_set_lean_p3(0)
+        return self
+
+    def __exit__(self, *exc):
+        _lib.pam_set_lean_p3(1)
+        return False

@@ -75,6 +75,36 @@ def test_tie_warning_f64(cuda, pam, orc, n, geom):
         assert bool(st[r] & TIE) == bool(orc.tie_warning(x[r]))
 
 
+def test_tie_warning_undecided_overflow(cuda, pam, orc):
+    """The fp64 screen works on 32-bit order keys (sign, exponent, 20 mantissa
+    bits); rows whose top-2 keys straddle the 1e-9 threshold are settled by an
+    exact re-scan at the end of the kernel from a 16-entry queue per cluster, or
+    by re-scanning every row of the cluster when the queue overflows.  Every
+    row here is undecided (duplicated maxima, sub-ulp-of-key gaps on both sides
+    of 1e-9), ~20 per cluster at n = 151936."""
+    torch = cuda
+    B, n = 300, 151936
+    rng = np.random.default_rng(77)
+    x = rng.normal(0.0, 3.0, size=(B, n))
+    gaps = [0.0, 5e-10, 9.99e-10, 1.001e-9, 3e-9, 0.0]
+    for r in range(B):
+        i, j = rng.choice(n, size=2, replace=False)
+        top = x[r].max() + 1.0
+        x[r, i] = top
+        x[r, j] = top - gaps[r % len(gaps)]
+    xt = torch.as_tensor(x, device="cuda")
+    with pam.geometry_override(8, 512, 34, 9):  # 15 clusters: 20 rows each
+        z, am, st = pam.cutmax_batch_device(xt, pam.CutMaxParams())
+        info = pam.launch_info(8, B, n, pam.CutMaxParams())
+    torch.cuda.synchronize()
+    st = st.cpu().numpy()
+    assert np.all((st & 0xFF) == 0)
+    want = np.array([orc.tie_warning(x[r]) for r in range(B)])
+    assert np.array_equal((st & TIE) != 0, want != 0)
+    assert np.array_equal(am.cpu().numpy(), x.argmax(axis=1))
+    assert B / info["clusters"] > 16
+
+
 def test_tie_warning_f32_and_generic_p(cuda, pam, orc):
     x = tie_rows(56, 32768, seed=5, dtype=np.float32)
     prm = pam.CutMaxParams()

@@ -34,9 +34,17 @@ def seq(T):
 
 
 def run(B, n, dtype, cfg=None, T=4):
-    key = "PAM_FORCE_CFG_F64" if dtype == torch.float64 else "PAM_FORCE_CFG_F32"
+    """cfg: "NTGxExC[xMINB]" forces the geometry (pam_set_geometry_override)."""
+    import contextlib
+    ov = contextlib.nullcontext()
     if cfg:
-        os.environ[key] = cfg
+        g = [int(v) for v in cfg.split("x")]
+        ov = pam.geometry_override(8 if dtype == torch.float64 else 4, g[0], g[1], g[2], g[3] if len(g) > 3 else 0)
+    with ov:
+        _run(B, n, dtype, T)
+
+
+def _run(B, n, dtype, T):
     x = W.torch_gaussian(B, n, seed=1, dtype=dtype)
     prm = pam.CutMaxParams(T=T)
     info = pam.launch_info(x.element_size(), B, n, prm)
@@ -71,14 +79,12 @@ def run(B, n, dtype, cfg=None, T=4):
               f"p90 {np.percentile(d, 90):6.0f}")
     print(f"   {'-> next row start':28s} {np.median(tr[:, 2:8, 0] - tr[:, 1:7, 21]):8.0f} cyc")
     print(f"   {'row period':28s} {period:8.0f} cyc  {period / CLK:6.2f} us")
-    os.environ.pop(key, None)
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "nostore":
-        run(4096, 151936, torch.float64)
-        os.environ["PAM_DEBUG_FLAGS"] = "1"
-        run(4096, 151936, torch.float64)
+    if len(sys.argv) > 1:  # n B cfg...
+        for c in sys.argv[3:] or [None]:
+            run(int(sys.argv[2]), int(sys.argv[1]), torch.float64, c)
         sys.exit(0)
     run(4096, 151936, torch.float64)
     run(4096, 32768, torch.float64)
