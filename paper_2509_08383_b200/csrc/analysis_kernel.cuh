@@ -57,8 +57,8 @@ __device__ __forceinline__ void analysis_init(ControlBlock* cb, uint32_t C) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 32u);
-    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 32u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * kXchBytes);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * kXchBytes);
   }
   ptx::cluster_sync();
 }

@@ -48,6 +48,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <stdio.h>
 #include <cuda_runtime.h>
 
 #include "../../include/pam_c_api.h"
@@ -87,7 +88,33 @@ struct CutmaxArgs {
 struct __align__(16) XchRecord {
   double2 ab;
   double2 cand;  // (value, index bits)
+#ifdef PAM_CHECKED_BUILD
+  double2 tag;   // checked build: (round, sender rank), verified by the receiver
+#endif
 };
+// tx bytes one sender completes on a receiver's exchange mbarrier
+#ifdef PAM_CHECKED_BUILD
+constexpr uint32_t kXchBytes = 48;
+#else
+constexpr uint32_t kXchBytes = 32;
+#endif
+
+// Checked build (make checked -> libpam_checked.so; compute-sanitizer is closed
+// on the GPU pool): protocol and bounds assertions that trap with a message.
+#ifdef PAM_CHECKED_BUILD
+#define PAM_CHECK(cond)                                                                                  \
+  do {                                                                                                   \
+    if (!(cond)) {                                                                                       \
+      printf("PAM_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                          \
+      __trap();                                                                                          \
+    }                                                                                                    \
+  } while (0)
+#else
+#define PAM_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 // Coefficients the control warp publishes for the next pass (p = 3 flow).
 struct __align__(16) Bcast {
@@ -497,6 +524,10 @@ __device__ __forceinline__ void xch_push(double a, double b, double c, long long
       ptx::st_async_f64x2(ptx::mapa(ptx::smem_addr(&cb->xch[par][rank].ab), (uint32_t)lane), ca, cbv, bar);
       ptx::st_async_b64x2(ptx::mapa(ptx::smem_addr(&cb->xch[par][rank].cand), (uint32_t)lane),
                           (uint64_t)__double_as_longlong(cv), (uint64_t)cix, bar);
+#ifdef PAM_CHECKED_BUILD
+      ptx::st_async_b64x2(ptx::mapa(ptx::smem_addr(&cb->xch[par][rank].tag), (uint32_t)lane), (uint64_t)round,
+                          (uint64_t)rank, bar);
+#endif
     }
     if (t2.on) t2_send<NW>(cb, lane, rank, C, t2);
   } else if (warp == NW - 1 && lane == 0) {
@@ -513,10 +544,16 @@ __device__ __forceinline__ double2 xch_wait(double& c, long long& ci, Ch* cb, ui
   const int lane = gtid & 31;
   const uint32_t par = round & 1u, ph = (round >> 1) & 1u;
   ptx::mbar_wait_cta(ptx::smem_addr(&cb->mb_x[par]), ph);
-  if (gtid == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[par]), C * 32u);  // arm round+2
+  if (gtid == 0) ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[par]), C * kXchBytes);  // arm round+2
   const int src = lane & 15;
   const bool have = src < (int)C;
   const XchRecord rec = cb->xch[par][have ? src : 0];
+#ifdef PAM_CHECKED_BUILD
+  if (have) {  // the record of every sender is this round's
+    PAM_CHECK((uint64_t)__double_as_longlong(rec.tag.x) == (uint64_t)round);
+    PAM_CHECK((uint64_t)__double_as_longlong(rec.tag.y) == (uint64_t)src);
+  }
+#endif
   double a = have ? rec.ab.x : (MODE == kTop2 ? -HUGE_VAL : 0.0);
   double b = have ? rec.ab.y : (MODE == kTop2 ? -HUGE_VAL : 0.0);
   if (MODE == kTop2)
@@ -1057,19 +1094,29 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
   }
   __syncthreads();
   if (gtid == 0) {
-    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 32u);
-    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 32u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * kXchBytes);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * kXchBytes);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_in), C * 16u);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[0]), C * 16u);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[1]), C * 16u);
   }
   ptx::cluster_sync();
 
+#ifdef PAM_CHECKED_BUILD
+  PAM_CHECK(len <= NTG * E && a.L <= NTG * E);
+  if (TMA) {
+    PAM_CHECK(len % VEC == 0 && (uintptr_t)a.x % 16 == 0 && (uintptr_t)a.z % 16 == 0 && a.ldx % VEC == 0);
+    for (int i = gtid; i < NTG * E; i += NTG) buf[i] = Elem(NAN);  // poison (see cutmax_p3_kernel.cuh)
+    ptx::fence_proxy_async_smem();
+  }
+  __syncthreads();
+#endif
   // ---- DMA-thread helpers ----------------------------------------------------
   auto load_chunk = [&](int64_t row, int i) {
     const unsigned char* src = reinterpret_cast<const unsigned char*>(X + row * a.ldx + base);
     const uint32_t off = (uint32_t)i * chunk;
     const uint32_t nb = (slice_bytes - off) < chunk ? (slice_bytes - off) : chunk;
+    PAM_CHECK(row >= 0 && row < a.B && ((uintptr_t)(src + off) & 15) == 0 && nb % 16 == 0);
     ptx::bulk_g2s(ptx::smem_addr(buf) + off, src + off, nb, bar_load, policy);
   };
   auto store_all = [&](int64_t row) {  // buf -> Z(row), one bulk group per chunk

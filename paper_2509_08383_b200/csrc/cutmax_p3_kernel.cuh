@@ -76,17 +76,25 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_p3_kernel(const CutmaxArgs a) {
   }
   __syncthreads();
   if (gtid == 0) {
-    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * 32u);
-    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * 32u);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[0]), C * kXchBytes);
+    ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_x[1]), C * kXchBytes);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[0]), C * 16u);
     ptx::mbar_arrive_expect_tx(ptx::smem_addr(&cb->mb_t[1]), C * 16u);
   }
   ptx::cluster_sync();
+#ifdef PAM_CHECKED_BUILD
+  PAM_CHECK(len <= NTG * E && len % VEC == 0 && a.L % VEC == 0 && a.L <= NTG * E);
+  PAM_CHECK((uintptr_t)a.x % 16 == 0 && (uintptr_t)a.z % 16 == 0 && a.ldx % VEC == 0 && a.ldz % VEC == 0);
+  for (int i = gtid; i < NTG * E; i += NTG) buf[i] = Elem(NAN);  // poison: reading an unlanded row gives NaN
+  ptx::fence_proxy_async_smem();
+  __syncthreads();
+#endif
 
   auto load_chunk = [&](int64_t r, int i) {
     const unsigned char* src = reinterpret_cast<const unsigned char*>(X + r * a.ldx + base);
     const uint32_t off = (uint32_t)i * chunk;
     const uint32_t nb = (slice_bytes - off) < chunk ? (slice_bytes - off) : chunk;
+    PAM_CHECK(r >= 0 && r < a.B && ((uintptr_t)(src + off) & 15) == 0 && nb % 16 == 0 && off + nb <= slice_bytes);
     ptx::bulk_g2s(ptx::smem_addr(buf) + off, src + off, nb, bar_load, policy);
   };
   auto store_all = [&](int64_t r) {  // buf -> Z(r), one bulk group per chunk
@@ -94,6 +102,7 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_p3_kernel(const CutmaxArgs a) {
     for (int i = 0; i < nch; ++i) {
       const uint32_t off = (uint32_t)i * chunk;
       const uint32_t nb = (slice_bytes - off) < chunk ? (slice_bytes - off) : chunk;
+      PAM_CHECK(r >= 0 && r < a.B && ((uintptr_t)(dst + off) & 15) == 0 && nb % 16 == 0);
       ptx::bulk_s2g(dst + off, ptx::smem_addr(buf) + off, nb, policy);
       ptx::bulk_commit();
     }
