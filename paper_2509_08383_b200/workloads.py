@@ -49,6 +49,19 @@ def zipf_logits(B: int, n: int, seed: int, s: float = 1.1, noise: float = 0.5) -
     return x
 
 
+def peaked_logits(B: int, n: int, seed: int, min_gap: float = 0.05) -> np.ndarray:
+    """SPEC.md:606's "peaked fixture vectors": the LLM-like Zipf rows above with
+    the top-1 logit margin raised to at least `min_gap` (nats) where the noise
+    left a near-tie; the paper's logits (QWEN, Table 1) are not available."""
+    x = zipf_logits(B, n, seed)
+    for r in range(B):
+        i = int(np.argmax(x[r]))
+        second = np.partition(x[r], -2)[-2]
+        if x[r, i] - second < min_gap:
+            x[r, i] = second + min_gap
+    return x
+
+
 def torch_gaussian(B: int, n: int, seed: int, dtype=None, device="cuda", sigma: float = 3.0):
     """Device-side N(0, sigma^2) generator for bench-scale inputs (GBs)."""
     import torch

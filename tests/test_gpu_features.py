@@ -262,3 +262,40 @@ def test_c5_full_batch_every_row(cuda, pam, orc, n, dtype):
         check(z[r0:r0 + 512].cpu().numpy(), am[r0:r0 + 512].cpu().numpy(), st[r0:r0 + 512].cpu().numpy(),
               zr, amr, str_, tol)
         assert np.array_equal(amr, np.argmax(xh, axis=1))
+
+
+# ---------------------------------------------------- SPEC acceptance #1 ----
+@pytest.mark.parametrize("n", [50257, 151936])
+def test_acceptance_argmax_recovery_table1(cuda, pam, orc, n):
+    """SPEC.md:606 (acceptance #1; Table 1): on 100 peaked
+    LLM-like fixtures (workloads.peaked_logits: log Zipf(1.1) + N(0, 0.5^2),
+    permuted, top-1 margin >= 0.05 nats; the paper's QWEN logits are
+    unavailable, SPEC.md:601) cutmax with (T, p, c) = (4, 13, 15) and (5, 9, 15)
+    recovers the argmax in 100/100 rows, with mean top mass >= 0.999 (T = 4) and
+    >= 1 - 1e-6 (T = 5), in < 10 s.  On the raw Zipf rows (near-ties allowed)
+    the argmax is still recovered 100/100; their top mass is lower on the
+    near-tie rows and equals the oracle's.  8 rows per setting are checked
+    against the oracle (tolerance 1e-12 * p^T / 81)."""
+    import time
+
+    torch = cuda
+    for peaked in (True, False):
+        x = W.peaked_logits(100, n, seed=606) if peaked else W.zipf_logits(100, n, seed=606)
+        xt = torch.as_tensor(x, device="cuda")
+        for T, p, c, mass in ((4, 13, 15.0, 0.999), (5, 9, 15.0, 1.0 - 1e-6)):
+            prm = pam.CutMaxParams(T=T, p=p, c=c)
+            t0 = time.perf_counter()
+            z, am, st = pam.cutmax_batch_device(xt, prm)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            assert dt < 10.0
+            st = st.cpu().numpy()
+            assert np.all((st & 0xFF) == 0)
+            assert np.array_equal(am.cpu().numpy(), x.argmax(axis=1)), "argmax recovery < 100/100"
+            top = z.max(dim=1).values.cpu().numpy()
+            print(f"n={n} peaked={peaked} (T,p,c)=({T},{p},{c}): mean top mass {top.mean():.9f}, "
+                  f"min {top.min():.9f}, {dt * 1e3:.1f} ms")
+            if peaked:
+                assert top.mean() >= mass
+            zr, amr, sr = orc.cutmax_batch(x[:8], prm.lower())
+            check(z[:8].cpu().numpy(), am[:8].cpu().numpy(), st[:8], zr, amr, sr, TOL64 * p ** T / 81)
