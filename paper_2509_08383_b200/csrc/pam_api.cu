@@ -16,6 +16,7 @@
 #include "../../include/pam_c_api.h"
 #include "analysis_kernel.cuh"
 #include "cutmax_kernel.cuh"
+#include "cutmax_warp_kernel.cuh"
 #include "nucleus_kernel.cuh"
 #include "pam_variants.h"
 #include "pam_scalar.h"
@@ -265,6 +266,44 @@ int fill_row_params(const pam_cutmax_params* prm, RowParams* rp) {
   return PAM_OK;
 }
 
+// ---- warp-per-row kernels ------------------------------------------------------
+constexpr int kWarpBlock = 256;  // 8 rows in flight per CTA
+// smallest compiled E that holds the row; none for early stopping (general kernel)
+// or when the specialised kernels are switched off (pam_set_lean_p3(0), A/B tests)
+const WarpVariant* pick_warp_variant(int elem_bytes, int64_t n, int flavour) {
+  if (flavour == 2 || !g_ovr.lean.load() || g_ovr.ntg[elem_bytes == 8 ? 1 : 0].load() > 0) return nullptr;
+  const WarpVariant* best = nullptr;
+  for (int i = 0; i < kNumWarpVariants; ++i) {
+    const WarpVariant& w = kWarpVariants[i];
+    if (w.elem_bytes == elem_bytes && 32 * (int64_t)w.e >= n && (!best || w.e < best->e)) best = &w;
+  }
+  return best;
+}
+int warp_kernel_blocks(const void* fn, int64_t B) {
+  const int dev = current_device();
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void*>, int>> cache;  // (dev, fn) -> resident blocks
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& kv : cache)
+      if (kv.first.first == dev && kv.first.second == fn) per_sm = kv.second;
+  }
+  if (per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWarpBlock, 0) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    cache.push_back({{dev, fn}, per_sm});
+  }
+  int nsm = 148;
+  if (dev >= 0 && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
+  const int64_t want = (B + kWarpBlock / 32 - 1) / (kWarpBlock / 32);
+  const int64_t cap = (int64_t)per_sm * nsm;
+  return (int)(want < cap ? want : cap);
+}
+
 template <typename Elem>
 int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const pam_cutmax_params* prm, Elem* d_z,
                       int64_t ld_z, int32_t* d_argmax, int32_t* d_status, double* d_stats, cudaStream_t stream) {
@@ -278,6 +317,32 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   const bool tma = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_z % 16 == 0) && (ld_x % vec == 0) &&
                    (ld_z % vec == 0) && (n % vec == 0);
   const int flavour = flavour_of(prm);
+  CutmaxArgs ka;
+  memset(&ka, 0, sizeof ka);
+  ka.x = d_x;
+  ka.z = d_z;
+  ka.argmax = d_argmax;
+  ka.status = d_status;
+  ka.stats = d_stats;
+  ka.ldx = ld_x;
+  ka.ldz = ld_z;
+  ka.B = B;
+  ka.n = n;
+  ka.tma = tma ? 1 : 0;
+  ka.inv_n = 1.0 / (double)n;
+  fill_row_params(prm, &ka.rp);
+  // short rows: one warp per row (cutmax_warp_kernel.cuh), no cluster
+  const WarpVariant* wv = tma ? pick_warp_variant((int)sizeof(Elem), n, flavour) : nullptr;
+  if (wv) {
+    const void* wfn = wv->fn[n == 32 * (int64_t)wv->e ? 1 : 0][flavour == 1 ? 1 : 0];
+    const int blocks = warp_kernel_blocks(wfn, B);
+    if (blocks <= 0) return cuda_fail(cudaErrorInvalidConfiguration, "warp kernel occupancy 0");
+    const void* args[] = {&ka};
+    cudaError_t e = cudaLaunchKernel(wfn, dim3((unsigned)blocks), dim3(kWarpBlock), (void**)args, 0, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel(warp rows)");
+    g_launches.fetch_add(1);
+    return PAM_OK;
+  }
   const Geometry g = choose_geometry((int)sizeof(Elem), B, n, flavour);
   if (!g.var) return PAM_ERR_UNSUPPORTED;
   const void* fn = g.var->fn[flavour];
@@ -295,23 +360,9 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   const int maxcl = max_active_clusters(fn, nt, g.C, smem);
   if (maxcl <= 0) return cuda_fail(cudaErrorInvalidConfiguration, "no cluster fits (occupancy 0)");
   const int clusters = (int)(B < maxcl ? B : maxcl);
-  CutmaxArgs ka;
-  memset(&ka, 0, sizeof ka);
-  ka.x = d_x;
-  ka.z = d_z;
-  ka.argmax = d_argmax;
-  ka.status = d_status;
-  ka.stats = d_stats;
-  ka.ldx = ld_x;
-  ka.ldz = ld_z;
-  ka.B = B;
-  ka.n = n;
   ka.L = g.L;
   ka.ctrl_offset = buffer_bytes(*g.var);
-  ka.tma = tma ? 1 : 0;
-  ka.inv_n = 1.0 / (double)n;
   if (g_trace && (int64_t)clusters * g.C * kTraceRows * kTraceEvents <= g_trace_entries) ka.trace = g_trace;
-  fill_row_params(prm, &ka.rp);
   return launch_cluster_kernel(fn, nt, g.C, clusters, smem, stream, &ka);
 }
 
@@ -690,6 +741,18 @@ int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_par
   if (!info || (dtype_bytes != 4 && dtype_bytes != 8)) return PAM_ERR_BAD_ARGUMENT;
   memset(info, 0, sizeof *info);
   const int flavour = prm ? flavour_of(prm) : 1;
+  if (const WarpVariant* wv = pick_warp_variant(dtype_bytes, n, flavour)) {  // warp per row
+    const int blocks = warp_kernel_blocks(wv->fn[n == 32 * (int64_t)wv->e ? 1 : 0][flavour == 1 ? 1 : 0], B);
+    info->threads = 32;
+    info->elems_per_thread = wv->e;
+    info->cluster = 1;
+    info->clusters = (int)(B < (int64_t)blocks * (kWarpBlock / 32) ? B : (int64_t)blocks * (kWarpBlock / 32));
+    info->ctas = blocks;
+    info->tma = 0;
+    info->groups = 1;
+    info->kernel_id = 2000 + (int)(wv - kWarpVariants) + 100 * flavour;
+    return PAM_OK;
+  }
   const Geometry g = choose_geometry(dtype_bytes, B, n, flavour);
   if (!g.var) return PAM_ERR_UNSUPPORTED;
   const void* fn = g.var->fn[flavour];

@@ -39,6 +39,14 @@ struct LeanVariant {
   int elem_bytes, ntg, e, minb;
   const void* fn;
 };
+// Warp-per-row kernels (cutmax_warp_kernel.cuh): rows of n <= 32 * e elements.
+struct WarpVariant {
+  int elem_bytes, e;
+  const void* fn[2][2];  // [n == 32 * e][p = 3 everywhere]
+};
+extern const WarpVariant kWarpVariants[];
+extern const int kNumWarpVariants;
+
 extern const LeanVariant kCutmaxP3F64[];
 extern const int kNumCutmaxP3F64;
 
