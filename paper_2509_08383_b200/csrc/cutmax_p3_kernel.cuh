@@ -1,5 +1,6 @@
-// cutmax_p3_kernel.cuh — lean batched CutMax for the headline schedule: odd
-// power p = 3 at every iteration, T >= 2, 16-byte aligned rows (TMA path).
+// cutmax_p3_kernel.cuh — lean batched CutMax for a fixed odd power at every
+// iteration (p = 3, the headline schedule, and the Table-1 powers 5, 9, 13, 19;
+// PAPER.md:277-280), T >= 2, 16-byte aligned rows (TMA path).
 //
 // Replaces core.cutmax for those parameters (Alg. 1
 // PAPER.md:51-72); every other case runs cutmax_rows_kernel (cutmax_kernel.cuh),
@@ -25,8 +26,12 @@
 
 namespace pam {
 
-template <typename Elem, int NTG, int E>
-__global__ void __launch_bounds__(NTG, 1) cutmax_p3_kernel(const CutmaxArgs a) {
+// P: the odd power at every iteration (3: analytic normaliser; other P: an
+// explicit sum of Y^(T+1) -- one more pass and exchange -- before the fused
+// last pass).
+template <typename Elem, int NTG, int E, int MINB = 0, int P = 3>
+__global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, NTG, E>()))
+    cutmax_lean_kernel(const CutmaxArgs a) {
   using Tr = ElemTraits<Elem>;
   using V = typename Tr::V;
   constexpr int VEC = Tr::VEC;
@@ -269,6 +274,10 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_p3_kernel(const CutmaxArgs a) {
       bd = fma(-dm, kd, 1.0);
       rn = 1.0;
       if (t == T - 1) {
+        if (P != 3) {  // no closed form: the CTA sums Y^(T+1) explicitly
+          rn = NAN;
+          return;
+        }
         const double nd = (double)a.n;
         const double total = nd + kd * (3.0 * e1 + kd * (3.0 * nd * s2 + kd * nd * m3));
         if (st == PAM_OK && !isfinite(total)) {
@@ -292,7 +301,7 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_p3_kernel(const CutmaxArgs a) {
         const double qn = Q * inv_n;
         double s2 = fma(-dm, dm, qn);
         double e1 = 0.0, m3 = 0.0;
-        if (last) {
+        if (last && P == 3) {
           e1 = fma(-nd, dm, S);
           m3 = fma(dm, fma(2.0 * dm, dm, -3.0 * qn), cb->p3_R * inv_n);
         }
@@ -368,14 +377,14 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_p3_kernel(const CutmaxArgs a) {
       control(t, ke, be, re_unused);
       const Elem kn = (Elem)(-a.rp.kshift[t + 1]);
       PAM_TRACE(tr, 13 + t);
-      const bool need3 = (t + 2 == T);
+      const bool need3 = (P == 3) && (t + 2 == T);
       Elem sa = 0, sb = 0, qa = 0, qb = 0, ra = 0, rb = 0;
       auto pass = [&](auto r3_c) {
         constexpr bool R3 = decltype(r3_c)::value;
 #pragma unroll
         for (int i = 0; i < E; i += 2) {
-          const Elem d0 = cutmax_update<Elem, 3>(v[i], ke, be, kn, 3);
-          const Elem d1 = cutmax_update<Elem, 3>(v[i + 1], ke, be, kn, 3);
+          const Elem d0 = cutmax_update<Elem, P>(v[i], ke, be, kn, P);
+          const Elem d1 = cutmax_update<Elem, P>(v[i + 1], ke, be, kn, P);
           v[i] = d0;
           v[i + 1] = d1;
           if (R3) {
@@ -432,7 +441,7 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_p3_kernel(const CutmaxArgs a) {
         long long ci = 0;
         const double2 r = need3 ? xch_wait<kSum3>(r3, ci, cb, xround, C, gtid)
                                 : xch_wait<kSum2>(r3, ci, cb, xround, C, gtid);
-        const double wd = (double)cutmax_update<Elem, 3>((Elem)cb->p3_w, ke, be, kn, 3);
+        const double wd = (double)cutmax_update<Elem, P>((Elem)cb->p3_w, ke, be, kn, P);
         const double m = mph();
         __syncwarp();
         if (gtid == 0) {
@@ -452,18 +461,18 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_p3_kernel(const CutmaxArgs a) {
     Elem ke, be, re;
     control(T - 1, ke, be, re);
     const Elem kz = (Elem)0;  // kshift[T] = 0
-    if (!(re == re)) {  // analytic total not finite: explicit sum of Y (rare, cluster-uniform)
+    if (!(re == re)) {  // explicit sum of Y: P != 3, or the analytic total is not finite (rare); cluster-uniform
       Elem ta = 0, tb = 0;
 #pragma unroll
       for (int i = 0; i < E; i += 2) {
-        const Elem y0 = cutmax_update<Elem, 3>(v[i], ke, be, kz, 3);
-        const Elem y1 = cutmax_update<Elem, 3>(v[i + 1], ke, be, kz, 3);
+        const Elem y0 = cutmax_update<Elem, P>(v[i], ke, be, kz, P);
+        const Elem y1 = cutmax_update<Elem, P>(v[i + 1], ke, be, kz, P);
         if (real(i)) ta += y0;
         if (real(i + 1)) tb += y1;
       }
       const double tot = cluster_sum2<NTG>((double)ta + (double)tb, 0.0, cb, xround, rank, C, gtid).x;
       if (warp == 0) {
-        const double total = tot - mph() * (double)cutmax_update<Elem, 3>((Elem)cb->p3_w, ke, be, kz, 3);
+        const double total = tot - mph() * (double)cutmax_update<Elem, P>((Elem)cb->p3_w, ke, be, kz, P);
         int st = cb->p3_st;
         const double rn = finish_total(total, st);
         __syncwarp();
@@ -499,7 +508,7 @@ __global__ void __launch_bounds__(NTG, 1) cutmax_p3_kernel(const CutmaxArgs a) {
         Elem o[VEC];
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          const Elem y = cutmax_update<Elem, 3>(v[kk * VEC + j], ke, be, kz, 3);
+          const Elem y = cutmax_update<Elem, P>(v[kk * VEC + j], ke, be, kz, P);
           if (y > bestv) {  // slots in increasing element order: strict > keeps the lowest index
             bestv = y;
             besto = kk * VEC + j;

@@ -266,6 +266,29 @@ int fill_row_params(const pam_cutmax_params* prm, RowParams* rp) {
   return PAM_OK;
 }
 
+// The odd power used at every iteration, or 0 for a mixed schedule.
+int uniform_p(const pam_cutmax_params* prm) {
+  for (int t = 1; t < prm->T; ++t)
+    if (prm->p[t] != prm->p[0]) return 0;
+  return prm->p[0];
+}
+
+// Lean kernel (cutmax_p3_kernel.cuh) of a general-kernel geometry for one fixed
+// power p at every iteration (nullptr: none compiled).  Used for T >= 2,
+// aligned rows, no early stopping, unless switched off (pam_set_lean_p3(0)).
+const LeanVariant* find_lean(int elem_bytes, const Variant& v, int p) {
+  if (!g_ovr.lean.load() || p <= 0) return nullptr;
+  const LeanVariant* tabs[2] = {elem_bytes == 8 ? kCutmaxP3F64 : kCutmaxP3F32,
+                                elem_bytes == 8 ? kCutmaxPGenF64 : nullptr};
+  const int cnts[2] = {elem_bytes == 8 ? kNumCutmaxP3F64 : kNumCutmaxP3F32, elem_bytes == 8 ? kNumCutmaxPGenF64 : 0};
+  for (int k = 0; k < 2; ++k)
+    for (int i = 0; i < cnts[k]; ++i) {
+      const LeanVariant& l = tabs[k][i];
+      if (l.p == p && l.ntg == v.ntg && l.e == v.e && l.minb == v.minb) return &l;
+    }
+  return nullptr;
+}
+
 // ---- warp-per-row kernels ------------------------------------------------------
 constexpr int kWarpBlock = 256;  // 8 rows in flight per CTA
 // smallest compiled E that holds the row; none for early stopping (general kernel)
@@ -347,12 +370,8 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   if (!g.var) return PAM_ERR_UNSUPPORTED;
   const void* fn = g.var->fn[flavour];
   // p = 3 everywhere, T >= 2, aligned rows: the lean kernel of the same geometry
-  if (flavour == 1 && tma && prm->T >= 2 && sizeof(Elem) == 8 && g_ovr.lean.load()) {
-    for (int i = 0; i < kNumCutmaxP3F64; ++i) {
-      const LeanVariant& lv = kCutmaxP3F64[i];
-      if (lv.ntg == g.var->ntg && lv.e == g.var->e && lv.minb == g.var->minb) fn = lv.fn;
-    }
-  }
+  if (flavour != 2 && tma && prm->T >= 2)
+    if (const LeanVariant* lv = find_lean((int)sizeof(Elem), *g.var, uniform_p(prm))) fn = lv->fn;
   // the row buffer is sized for the full capacity even without TMA so the
   // occupancy (and the chooser's estimate) does not depend on alignment
   const int smem = smem_bytes(*g.var);
@@ -768,10 +787,8 @@ int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_par
   info->groups = 1;
   const VariantTable& tab = kCutmaxTables[dtype_bytes == 8 ? 1 : 0];
   info->kernel_id = (int)(g.var - tab.v) + 100 * flavour;
-  if (flavour == 1 && dtype_bytes == 8 && prm->T >= 2 && g_ovr.lean.load())
-    for (int i = 0; i < kNumCutmaxP3F64; ++i)
-      if (kCutmaxP3F64[i].ntg == g.var->ntg && kCutmaxP3F64[i].e == g.var->e && kCutmaxP3F64[i].minb == g.var->minb)
-        info->kernel_id += 1000;  // lean p = 3 kernel (aligned rows)
+  if (flavour != 2 && prm && prm->T >= 2 && find_lean(dtype_bytes, *g.var, uniform_p(prm)))
+    info->kernel_id += 1000;  // lean kernel (aligned rows)
   return PAM_OK;
 }
 

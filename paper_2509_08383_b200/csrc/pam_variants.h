@@ -36,7 +36,7 @@ struct SamplerVariant {
 // Lean p = 3 kernels (cutmax_p3_kernel.cuh), matched to a Variant by
 // (elem_bytes, ntg, e, minb).
 struct LeanVariant {
-  int elem_bytes, ntg, e, minb;
+  int elem_bytes, ntg, e, minb, p;  // p: the odd power at every iteration
   const void* fn;
 };
 // Warp-per-row kernels (cutmax_warp_kernel.cuh): rows of n <= 32 * e elements.
@@ -49,6 +49,10 @@ extern const int kNumWarpVariants;
 
 extern const LeanVariant kCutmaxP3F64[];
 extern const int kNumCutmaxP3F64;
+extern const LeanVariant kCutmaxP3F32[];
+extern const int kNumCutmaxP3F32;
+extern const LeanVariant kCutmaxPGenF64[];
+extern const int kNumCutmaxPGenF64;
 
 extern const Variant kCutmaxVariantsF64[];
 extern const int kNumCutmaxVariantsF64;

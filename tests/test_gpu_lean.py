@@ -13,7 +13,7 @@ from paper_2509_08383_b200 import workloads as W
 pytestmark = pytest.mark.gpu
 
 
-def both(torch, pam, x, prm, stats=False):
+def both(torch, pam, x, prm, stats=False, tol=1e-14):
     """Run both kernels.  They share the algebra and the exchanges; the lean
     kernel accumulates a row's input sums in one (sum, sum of squares) pair
     where the general kernel interleaves two, so results agree to the last
@@ -31,12 +31,12 @@ def both(torch, pam, x, prm, stats=False):
         if general:
             with pam.general_p3_kernel():
                 pam.cutmax_batch_device(x, prm, z=z, argmax=am, status=st, stats=sv)
-                kid = pam.launch_info(8, B, n, prm)["kernel_id"]
+                kid = pam.launch_info(x.element_size(), B, n, prm)["kernel_id"]
             assert kid < 1000
         else:
             pam.cutmax_batch_device(x, prm, z=z, argmax=am, status=st, stats=sv)
-            kid = pam.launch_info(8, B, n, prm)["kernel_id"]
-            assert kid >= 1000, "lean kernel not selected"
+            kid = pam.launch_info(x.element_size(), B, n, prm)["kernel_id"]
+            assert 1000 <= kid < 2000, "lean kernel not selected"
         torch.cuda.synchronize()
         outs.append((z, am, st, sv))
     (z0, a0, s0, v0), (z1, a1, s1, v1) = outs
@@ -44,8 +44,8 @@ def both(torch, pam, x, prm, stats=False):
     assert torch.equal(a0, a1), f"argmax differs: {(a0 != a1).nonzero()[:5].flatten().tolist()}"
     ok = (s0 & 0xFF) == 0
     if bool(ok.any()):
-        err = ((z0[ok] - z1[ok]).abs().amax(1) / z1[ok].abs().amax(1)).max().item()
-        assert err <= 1e-14, err
+        err = ((z0[ok].double() - z1[ok].double()).abs().amax(1) / z1[ok].double().abs().amax(1)).max().item()
+        assert err <= tol, err
     if stats and bool(ok.any()):  # mu to 1e-12 sigma (means sit near 0), s2 to 1e-12 relative
         a, b = v0[ok], v1[ok]
         sig = b[..., 1].clamp_min(0).sqrt()
@@ -55,7 +55,7 @@ def both(torch, pam, x, prm, stats=False):
 
 
 @pytest.mark.parametrize("B,n,T", [(64, 151936, 4), (40, 151936, 2), (33, 151936, 3), (256, 32768, 4),
-                                   (200, 32768, 3), (1000, 1024, 4), (37, 9000, 4), (5, 50000, 5)])
+                                   (200, 32768, 3), (37, 9000, 4), (5, 50000, 5)])
 def test_lean_equals_general_gaussian(cuda, pam, B, n, T):
     torch = cuda
     x = W.torch_gaussian(B, n, seed=B + n + T)
@@ -111,3 +111,45 @@ def test_lean_row_position_independent(cuda, pam):
             z1, a1, s1 = pam.cutmax_batch_device(x[r:r + 1].contiguous(), prm)
             torch.cuda.synchronize()
             assert torch.equal(z1[0], z[r]) and int(a1[0]) == int(am[r]) and int(s1[0]) == int(st[r])
+
+
+@pytest.mark.parametrize("B,n", [(64, 151936), (300, 32768), (40, 9000)])
+def test_lean_fp32_equals_general(cuda, pam, orc, B, n):
+    """fp32 rows (fp32 storage and elementwise math, fp64 statistics) on the lean
+    kernel vs the general one (2e-5 normwise: fp32 rounding of the two
+    accumulation orders: each is within the fp32 bar 1e-5 of the oracle, so
+    they agree to 2e-5), and 6 rows against the oracle at 1e-5."""
+    torch = cuda
+    x = W.torch_gaussian(B, n, seed=B + n, dtype=torch.float32)
+    z, am, st = both(torch, pam, x, pam.CutMaxParams(), tol=2e-5)
+    xs = x[:6].cpu().numpy()
+    zr, amr, sr = orc.cutmax_batch(xs, pam.CutMaxParams().lower())
+    zz = z[:6].cpu().numpy()
+    assert np.array_equal(am[:6].cpu().numpy(), amr) and np.array_equal(st[:6].cpu().numpy(), sr)
+    assert max(float(np.max(np.abs(zz[r] - zr[r])) / np.max(np.abs(zr[r]))) for r in range(6)) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [151936, 32768])
+@pytest.mark.parametrize("T,p,c", [(2, 19, 5.0), (3, 19, 27.0), (4, 13, 15.0), (5, 9, 15.0), (3, 5, 12.0)])
+def test_lean_table1_powers_vs_oracle(cuda, pam, orc, n, T, p, c):
+    """The lean kernel at the paper's Table-1 settings and
+    p = 5: explicit sum of Y^(T+1) instead of the p = 3 closed form.  Against the
+    oracle: argmax and status exact, Z within 1e-12 * p^T / 81 normwise (the
+    rounding amplification of test_gpu_parity.py)."""
+    torch = cuda
+    B = 24
+    x = W.zipf_logits(B, n, seed=T * 100 + p)
+    prm = pam.CutMaxParams(T=T, p=p, c=c)
+    xt = torch.as_tensor(x, device="cuda")
+    z, am, st = pam.cutmax_batch_device(xt, prm)
+    torch.cuda.synchronize()
+    assert 1000 <= pam.launch_info(8, B, n, prm)["kernel_id"] < 2000, "lean kernel not selected"
+    zr, amr, sr = orc.cutmax_batch(x, prm.lower())
+    st = st.cpu().numpy()
+    assert np.array_equal(st, sr)
+    ok = (st & 0xFF) == 0
+    assert np.array_equal(am.cpu().numpy()[ok], amr[ok])
+    zz = z.cpu().numpy()
+    tol = 1e-12 * max(1.0, p ** T / 81)
+    worst = max(float(np.max(np.abs(zz[r] - zr[r])) / np.max(np.abs(zr[r]))) for r in np.nonzero(ok)[0])
+    assert worst <= tol, worst

@@ -51,7 +51,7 @@ def kernel_name(info):
     k = info["kernel_id"]
     if k >= 2000:
         return f"warp/row E={info['elems_per_thread']}"
-    kind = "lean p3" if k >= 1000 else "general"
+    kind = "lean" if k >= 1000 else "general"
     return f"{kind} {info['threads']}x{info['elems_per_thread']} C={info['cluster']} cl={info['clusters']}"
 
 

@@ -30,27 +30,28 @@ def run(x, prm, reps=20):
 
 def main():
     n = int(sys.argv[1]); B = int(sys.argv[2])
-    dt = torch.float64
+    dt = torch.float32 if os.environ.get("GEO_F32") else torch.float64
+    esz = 4 if dt == torch.float32 else 8
     prm = pam.CutMaxParams()
     x = W.torch_gaussian(B, n, seed=1, dtype=dt)
     ms, z0, a0, s0 = run(x, prm)
-    info = pam.launch_info(8, B, n, prm)
-    gbs = B * (2 * n * 8 + 4) / ms / 1e6
+    info = pam.launch_info(esz, B, n, prm)
+    gbs = B * (2 * n * esz + 4) / ms / 1e6
     print(f"default {info['threads']}x{info['elems_per_thread']} C={info['cluster']}: {ms:.4f} ms {gbs:.0f} GB/s {100*gbs/PEAK:.1f}%")
     for g in sys.argv[3:]:
         parts = [int(v) for v in g.split("x")]
         ntg, e, c = parts[:3]
         mb = parts[3] if len(parts) > 3 else 0
         try:
-            with pam.geometry_override(8, ntg, e, c, mb):
+            with pam.geometry_override(esz, ntg, e, c, mb):
                 ms, z, a, s = run(x, prm)
-                info = pam.launch_info(8, B, n, prm)
+                info = pam.launch_info(esz, B, n, prm)
         except Exception as ex:  # noqa: BLE001
             print(g, "failed:", ex)
             continue
-        err = ((z - z0).abs().amax(1) / z0.abs().amax(1)).max().item()
+        err = ((z.double() - z0.double()).abs().amax(1) / z0.double().abs().amax(1)).max().item()
         same = bool(torch.equal(a, a0) and torch.equal(s, s0))
-        gbs = B * (2 * n * 8 + 4) / ms / 1e6
+        gbs = B * (2 * n * esz + 4) / ms / 1e6
         print(f"{g}: clusters={info['clusters']} {ms:.4f} ms {gbs:.0f} GB/s {100*gbs/PEAK:.1f}%  argmax/status same={same} normwise-vs-default={err:.1e}")
 
 
