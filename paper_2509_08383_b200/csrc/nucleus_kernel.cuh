@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
   const uint64_t policy = ptx::policy_evict_first();
 
   if (tid == 0) {
+    cb->unc_n = 0;
     ptx::mbar_init(bar_load, 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[0]), 1);
     ptx::mbar_init(ptx::smem_addr(&cb->mb_x[1]), 1);
@@ -152,7 +153,10 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
       __syncthreads();
     }
     double xmax = -HUGE_VAL;
-    double t1 = -HUGE_VAL, t2 = -HUGE_VAL;  // top-2 of x~ (TieWarning on the vector CutMax sees)
+    // TieWarning screen of x~ = x + G (the vector CutMax sees): top-2 high
+    // words on the FP32 pipe (cutmax_kernel.cuh: tie_decide), exact re-scan of
+    // undecided rows at the end of the kernel
+    float t1 = -INFINITY, t2 = -INFINITY;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const int li0 = (k * NT + tid) * VEC;
@@ -161,8 +165,8 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
         v[k * VEC + 0] = t.x + v[k * VEC + 0];  // Alg. 3 line 5: x~ = x + G
         v[k * VEC + 1] = t.y + v[k * VEC + 1];
         xmax = fmax(xmax, fmax(t.x, t.y));
-        top2_add(t1, t2, v[k * VEC + 0]);
-        top2_add(t1, t2, v[k * VEC + 1]);
+        top2f_add(t1, t2, hiword_f(v[k * VEC + 0]));
+        top2f_add(t1, t2, hiword_f(v[k * VEC + 1]));
       } else {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
             const double xv = buf[li0 + j];
             v[k * VEC + j] = xv + v[k * VEC + j];
             xmax = fmax(xmax, xv);
-            top2_add(t1, t2, v[k * VEC + j]);
+            top2f_add(t1, t2, hiword_f(v[k * VEC + j]));
           } else {
             v[k * VEC + j] = K0;  // phantom (see cutmax_iterate)
           }
@@ -183,7 +187,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     long long unused_argmax;
     const double2 part = input_pass<double, E>(v, K0);
     const double2 rin = cluster_sum2<NT>(part.x, part.y, cb, xround, rank, C, tid,
-                                         Top2Push{true, t1, t2, (uint32_t)(lrow & 1)});
+                                         KeyPush{true, fkey(t1), fkey(t2), (uint32_t)(lrow & 1)});
     auto final_xch = [&](double sy, double& bv, long long& bi) -> double {
       return cluster_reduce<NT, false>(sy, 0.0, bv, bi, cb, xround, rank, C, tid).x;
     };
@@ -299,11 +303,51 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     const double2 ta = cluster_sum2<NT>(tot, above, cb, xround, rank, C, tid);
     PAM_TRACE(tr, 5);
     if (warp == 0) {
-      const double2 tt = top2_wait(cb, (uint32_t)(lrow & 1), t2_ph, C, tid);
+      const int2 kk = top2k_wait(cb, (uint32_t)(lrow & 1), t2_ph, C, tid);
+      const int td = tie_decide<double>(st, kk.x, kk.y);
       if (rank == 0 && tid == 0) {
         if (a.token) a.token[row] = (st == PAM_OK) ? (int32_t)besti : -1;
         if (a.inside) a.inside[row] = (st == PAM_OK && ta.y < a.p_nucleus * ta.x) ? 1 : 0;
-        if (a.status) a.status[row] = st | tie_flag(st, tt);
+        if (a.status) a.status[row] = st | (td == 1 ? PAM_ROW_FLAG_TIE : 0);
+      }
+      if (td == 2 && tid == 0) {  // undecided (cluster-uniform): settled below
+        const int q = cb->unc_n;
+        if (q < 16) cb->unc_rows[q] = row;
+        cb->unc_n = q + 1;
+      }
+    }
+  }
+
+  // ---- TieWarning rows the screen left undecided: exact top-2 of x + G -------
+  // (rare: the two largest perturbed logits share their high word).  The noise
+  // is regenerated with the same functions as above, element pair by pair.
+  __syncthreads();
+  const int unc = cb->unc_n;
+  if (unc > 0 && a.status) {
+    const int64_t cnt = unc <= 16 ? unc : (a.B - cid + ncl - 1) / ncl;  // overflow: every row of the cluster
+    const bool fast = GUMBEL || a.inv_alpha <= 19.0;
+    for (int64_t j = 0; j < cnt; ++j) {
+      const int64_t r = unc <= 16 ? cb->unc_rows[j] : cid + j * ncl;
+      const double* xr = a.x + r * a.ldx + base;
+      const uint64_t key = a.seed ^ (uint64_t)r;
+      double m1 = -HUGE_VAL, m2 = -HUGE_VAL;
+      for (int i = 2 * tid; i < len; i += 2 * NT) {
+        double u0, u1;
+        uniform_pair(key, a.draw, (uint64_t)(base + i) >> 1, &u0, &u1);
+        const double us[2] = {u0, u1};
+        for (int q = 0; q < 2 && i + q < len; ++q) {
+          double g;
+          if (fast)
+            g = GUMBEL ? gumbel_fast(us[q]) : beta_icdf_fast(us[q], a.inv_alpha);
+          else
+            g = GUMBEL ? gumbel_from_u(us[q]) : beta_icdf(us[q], a.inv_alpha);
+          top2_add(m1, m2, xr[i + q] + g);
+        }
+      }
+      const double2 t = cluster_top2<NT>(m1, m2, cb, xround, rank, C, tid);
+      if (rank == 0 && tid == 0) {
+        const int s0 = a.status[r];
+        if ((s0 & 0xff) == PAM_OK) a.status[r] = (s0 & ~PAM_ROW_FLAG_TIE) | (t.x - t.y < 1e-9 ? PAM_ROW_FLAG_TIE : 0);
       }
     }
   }
