@@ -199,34 +199,47 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
     PAM_TRACE(tr, 3);
     // token = argmax of Y^(T+1) before the normalisation (pin A7, oracle.c
     // orc_cutmax: Y * inv(sum Y) could round a near-tie into an exact one);
-    // the optional one-hot output is Z = Y * rnorm
-    double best = -HUGE_VAL, bestx = 0.0;
-    long long besti = 0x7fffffffffffffffLL;
+    // the optional one-hot output is Z = Y * rnorm.  Each thread tracks its
+    // best register slot (compile-time immediates), x_tok is read once from
+    // the slot that wins; warps and the cluster combine with REDUX (warp_argmax).
+    double best = -HUGE_VAL;
+    int besto = -1;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const int li0 = (k * NT + tid) * VEC;
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
         const double y = v[k * VEC + j];
-        const double o = y * rnorm;
         if (li0 + j < len) {
-          if (y > best) {
+          if (y > best) {  // slots in increasing element order: strict > keeps the lowest index
             best = y;
-            besti = base + li0 + j;
-            bestx = buf[li0 + j];
+            besto = k * VEC + j;
           }
-          if (a.onehot) a.onehot[row * a.ld_onehot + base + li0 + j] = o;
+          if (a.onehot) a.onehot[row * a.ld_onehot + base + li0 + j] = y * rnorm;
         }
       }
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double ov = __shfl_down_sync(0xffffffffu, best, off);
-      const long long oi = __shfl_down_sync(0xffffffffu, besti, off);
-      const double ox = __shfl_down_sync(0xffffffffu, bestx, off);
-      if (cand_better(ov, oi, best, besti)) { best = ov; besti = oi; bestx = ox; }
-      xmax = fmax(xmax, __shfl_down_sync(0xffffffffu, xmax, off));
+    long long besti = 0x7fffffffffffffffLL;
+    double bestx = 0.0;
+    if (besto >= 0) {
+      const int li = ((besto / VEC) * NT + tid) * VEC + (besto % VEC);
+      besti = base + li;
+      bestx = buf[li];
     }
+    // warp: winner (value desc, index asc), its x, and max x
+    auto argmax_with_x = [&](double& bv, long long& bi, double& bx) {
+      const long long mine = bi;
+      warp_argmax(bv, bi);
+      const unsigned who = __ballot_sync(0xffffffffu, mine == bi);
+      bx = __shfl_sync(0xffffffffu, bx, who ? __ffs(who) - 1 : 0);
+    };
+    auto max_all = [&](double m) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+      return m;
+    };
+    argmax_with_x(best, besti, bestx);
+    xmax = max_all(xmax);
     if (lane == 0) cb->wred[warp] = make_double2(best, __longlong_as_double(besti));
     __shared__ double2 wx[32];
     if (lane == 0) wx[warp] = make_double2(bestx, xmax);
@@ -237,19 +250,8 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
       best = w.x;
       besti = __double_as_longlong(w.y);
       bestx = wxx.x;
-      xmax = wxx.y;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_down_sync(0xffffffffu, best, off);
-        const long long oi = __shfl_down_sync(0xffffffffu, besti, off);
-        const double ox = __shfl_down_sync(0xffffffffu, bestx, off);
-        if (cand_better(ov, oi, best, besti)) { best = ov; besti = oi; bestx = ox; }
-        xmax = fmax(xmax, __shfl_down_sync(0xffffffffu, xmax, off));
-      }
-      best = __shfl_sync(0xffffffffu, best, 0);
-      besti = __shfl_sync(0xffffffffu, besti, 0);
-      bestx = __shfl_sync(0xffffffffu, bestx, 0);
-      xmax = __shfl_sync(0xffffffffu, xmax, 0);
+      argmax_with_x(best, besti, bestx);
+      xmax = max_all(wxx.y);
       if (lane < (int)C) {  // all-gather: 32-byte record to every CTA
         const uint32_t bar = ptx::mapa(ptx::smem_addr(&cb->mb_g), (uint32_t)lane);
         ptx::st_async_b64x2(ptx::mapa(ptx::smem_addr(&cb->gat[rank][0]), (uint32_t)lane),
@@ -267,18 +269,8 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
       best = r0.x;
       besti = __double_as_longlong(r0.y);
       bestx = r1.x;
-      xmax = r1.y;
-#pragma unroll
-      for (int off = 8; off > 0; off >>= 1) {
-        const double ov = __shfl_down_sync(0xffffffffu, best, off);
-        const long long oi = __shfl_down_sync(0xffffffffu, besti, off);
-        const double ox = __shfl_down_sync(0xffffffffu, bestx, off);
-        if (cand_better(ov, oi, best, besti)) { best = ov; besti = oi; bestx = ox; }
-        xmax = fmax(xmax, __shfl_down_sync(0xffffffffu, xmax, off));
-      }
-      besti = __shfl_sync(0xffffffffu, besti, 0);
-      bestx = __shfl_sync(0xffffffffu, bestx, 0);
-      xmax = __shfl_sync(0xffffffffu, xmax, 0);
+      argmax_with_x(best, besti, bestx);
+      xmax = max_all(r1.y);
     }
 
     PAM_TRACE(tr, 4);
