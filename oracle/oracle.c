@@ -5,6 +5,7 @@
  * two roundings unless written as fma().
  */
 #include "oracle.h"
+#include "../paper_2509_08383_b200/csrc/pam_logexp_tables.h"
 
 #include <math.h>
 #include <stdlib.h>
@@ -189,17 +190,81 @@ double orc_uniform(uint64_t seed, uint64_t row, uint64_t draw, uint64_t i) {
   return ((double)(bits >> 12) + 0.5) * 0x1p-52;
 }
 
+/* Table-driven log / exp of the sampler's noise and nucleus test (the kernel's
+ * pam_scalar.h log_t / exp_t, restated operation for operation; tables from
+ * tools/gen_logexp_tables.py, 50-digit decimal, correctly rounded).
+ * log: x = 2^e m, m in [1,2); i = top 7 mantissa bits; m/2, e+1 for i >= 53;
+ * r = m * invc[i] - 1 (one rounding), log1p(r) to degree 8; + logc[i] + e ln2.
+ * exp: x = (128 q + j) ln2/128 + r (two-step Cody-Waite), exp(r)-1 to degree 5,
+ * 2^(j/128) (1 + (exp(r)-1)) with one rounding, times 2^q. */
+static const double orc_logt_invc[128] = {PAM_LOGT_INVC_VALUES};
+static const double orc_logt_logc[128] = {PAM_LOGT_LOGC_VALUES};
+static const double orc_expt_e2[128] = {PAM_EXPT_E2_VALUES};
+
+static double orc_bits_to_double(uint64_t b) { double d; memcpy(&d, &b, 8); return d; }
+static uint64_t orc_double_to_bits(double d) { uint64_t b; memcpy(&b, &d, 8); return b; }
+
+double orc_log_t(double x) {
+  if (x != x) return x;
+  if (x < 0.0) return NAN;
+  if (x == 0.0) return -INFINITY;
+  if (x > 1.79769313486231570815e308) return x;
+  uint64_t xb = orc_double_to_bits(x);
+  if ((xb >> 52) == 0) return orc_log(x);                     /* subnormal */
+  uint64_t mb = xb & 0x000fffffffffffffULL;
+  int i = (int)(mb >> 45);
+  int half = i >= 53;
+  int e = (int)(xb >> 52) - 1023 + (half ? 1 : 0);
+  double m = orc_bits_to_double(mb | 0x3ff0000000000000ULL);
+  if (half) m = m * 0.5;
+  double r = fma(m, orc_logt_invc[i], -1.0);
+  double a = fma(r, -0.125, 0x1.2492492492492p-3);
+  a = fma(a, r, -0x1.5555555555555p-3);
+  a = fma(a, r, 0x1.999999999999ap-3);
+  a = fma(a, r, -0.25);
+  a = fma(a, r, 0x1.5555555555555p-2);
+  a = fma(a, r, -0.5);
+  double lp = fma(r * r, a, r);
+  double t = orc_logt_logc[i] + lp;
+  double ed = (double)e;
+  return fma(ed, ORC_LN2_HI, fma(ed, ORC_LN2_LO, t));
+}
+
+double orc_exp_t(double x) {
+  if (x != x) return x;
+  if (x > 709.782712893383973096) return INFINITY;
+  if (x < -708.3964185322641) return 0.0;
+  double k = rint(x * 0x1.71547652b82fep+7);
+  double r = fma(-k, PAM_EXPT_LN2N_HI, x);
+  r = fma(-k, PAM_EXPT_LN2N_LO, r);
+  double p = fma(r, 0x1.1111111111111p-7, 0x1.5555555555555p-5);
+  p = fma(p, r, 0x1.5555555555555p-3);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  double em1 = r * p;
+  int ki = (int)k;
+  double tj = orc_expt_e2[ki & 127];
+  double y = fma(tj, em1, tj);
+  int q = ki >> 7;
+  if (q < -1021) {                       /* result may be subnormal: flush (as orc_exp) */
+    double tt = ldexp(y, q + 60);
+    return (tt < 0x1p-962) ? 0.0 : ldexp(tt, -60);
+  }
+  if (q > 1023) return ldexp(y, q - 1) * 2.0;
+  return ldexp(y, q);
+}
+
 /* betaInverseCdf u^(1/alpha) (Lemma 2 proof PAPER.md:208). */
 double orc_beta_icdf(double u, double alpha) {
   double inv_alpha = 1.0 / alpha;
   if (!(u > 0.0)) return 0.0;
   if (u >= 1.0) return 1.0;
   if (inv_alpha == 1.0) return u;
-  return orc_exp(orc_log(u) * inv_alpha);
+  return orc_exp_t(orc_log_t(u) * inv_alpha);
 }
 
 /* gumbelFromUniform -log(-log u) (Definition 1). */
-double orc_gumbel(double u) { return -orc_log(-orc_log(u)); }
+double orc_gumbel(double u) { return -orc_log_t(-orc_log_t(u)); }
 
 /* nucleusAlpha ln(1-q)/ln(p) (Observation 1 PAPER.md:212-215). */
 double orc_nucleus_alpha(double p, double q) {
@@ -577,7 +642,7 @@ int orc_nucleus_inside(const double* x, int64_t n, double p, int64_t tok) {
   for (i = 1; i < n; ++i) if (x[i] > m) m = x[i];
   double total = 0.0, above = 0.0, xt = x[tok];
   for (i = 0; i < n; ++i) {
-    double e = orc_exp(x[i] - m);
+    double e = orc_exp_t(x[i] - m);
     total += e;
     if (x[i] > xt) above += e;
   }

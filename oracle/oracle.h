@@ -52,6 +52,8 @@ double orc_exp(double x);
 double orc_log(double x);
 void   orc_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 double orc_uniform(uint64_t seed, uint64_t row, uint64_t draw, uint64_t i);
+double orc_log_t(double x);   /* table-driven log / exp of the sampler (pam_scalar.h log_t / exp_t) */
+double orc_exp_t(double x);
 double orc_beta_icdf(double u, double alpha);
 double orc_gumbel(double u);
 double orc_nucleus_alpha(double p, double q);

@@ -85,6 +85,8 @@ _SIG = {
     "orc_invsqrt_cfg": (C.c_int, [C.c_double, C.POINTER(_abi.pam_approx_config), C.POINTER(C.c_double)]),
     "orc_inv_cfg": (C.c_int, [C.c_double, C.POINTER(_abi.pam_approx_config), C.POINTER(C.c_double)]),
     "orc_exp": (C.c_double, [C.c_double]),
+    "orc_exp_t": (C.c_double, [C.c_double]),
+    "orc_log_t": (C.c_double, [C.c_double]),
     "orc_philox": (None, [_P, _P, _P]),
     "orc_log": (C.c_double, [C.c_double]),
     "orc_uniform": (C.c_double, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64]),

@@ -12,6 +12,8 @@
 //      and max(x) (one 32-byte record per CTA pushed to every CTA).
 //   5. One pass over x (shared memory): e = exp(x - max x), sums of e and of
 //      e over {x_k > x_tok}; one exchange; inside = above < p * total.
+// The noise and the nucleus exp use the table-driven log / exp of
+// pam_scalar.h (tables copied to shared memory once per CTA).
 // The noise is generated on chip and never stored; HBM traffic is 8n bytes
 // read per row plus 5 bytes written (+ 8n if the one-hot output is requested).
 #pragma once
@@ -19,6 +21,10 @@
 #include "cutmax_kernel.cuh"
 
 namespace pam {
+
+// shared memory after the row buffer: ControlBlock, then the log / exp tables
+constexpr int kSamplerTabOffset = ((int)sizeof(ControlBlock) + 15) / 16 * 16;
+constexpr int kSamplerTabBytes = 384 * 8;
 
 struct SamplerArgs {
   const double* x;
@@ -49,6 +55,9 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* buf = reinterpret_cast<double*>(smem_raw);
   ControlBlock* cb = reinterpret_cast<ControlBlock*>(smem_raw + a.ctrl_offset);
+  // log / exp tables (pam_scalar.h log_t_core / exp_t_core) in shared memory:
+  // invc[128], logc[128], e2[128] right after the control block
+  double* tabs = reinterpret_cast<double*>(smem_raw + a.ctrl_offset + kSamplerTabOffset);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -64,6 +73,11 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
   const uint32_t load_bytes = (uint32_t)len * 8u;
   const uint64_t policy = ptx::policy_evict_first();
 
+  for (int i = tid; i < 128; i += NT) {
+    tabs[i] = pam_d_logt_invc[i];
+    tabs[128 + i] = pam_d_logt_logc[i];
+    tabs[256 + i] = pam_d_expt_e2[i];
+  }
   if (tid == 0) {
     cb->unc_n = 0;
     ptx::mbar_init(bar_load, 1);
@@ -122,9 +136,10 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
         uniform_pair(key, a.draw, (uint64_t)(base + li1) >> 1, &u[2], &u[3]);
         double g[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) g[q] = GUMBEL ? -pam_log_fast(u[q]) : pam_log_fast(u[q]);
+        for (int q = 0; q < 4; ++q) g[q] = log_t_core(u[q], tabs, tabs + 128);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) g[q] = GUMBEL ? -pam_log_fast(g[q]) : pam_exp_fast(g[q] * a.inv_alpha);
+        for (int q = 0; q < 4; ++q)
+          g[q] = GUMBEL ? -log_t_core(-g[q], tabs, tabs + 128) : exp_t_core(g[q] * a.inv_alpha, tabs + 256);
         if (!GUMBEL && a.inv_alpha == 1.0) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) g[q] = u[q];
@@ -286,7 +301,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
           // exp(x - max) for x - max >= -700 (bit-identical branch-free form); below,
           // exp < 1e-304 cannot change the totals, which include exp(0) = 1
           const double d = xv - xmax;
-          const double e = d >= -700.0 ? pam_exp_fast(d) : (d == d ? 0.0 : d);
+          const double e = d >= -700.0 ? exp_t_core(d, tabs + 256) : (d == d ? 0.0 : d);
           tot += e;
           if (xv > bestx) above += e;
         }
@@ -317,7 +332,6 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
   const int unc = cb->unc_n;
   if (unc > 0 && a.status) {
     const int64_t cnt = unc <= 16 ? unc : (a.B - cid + ncl - 1) / ncl;  // overflow: every row of the cluster
-    const bool fast = GUMBEL || a.inv_alpha <= 19.0;
     for (int64_t j = 0; j < cnt; ++j) {
       const int64_t r = unc <= 16 ? cb->unc_rows[j] : cid + j * ncl;
       const double* xr = a.x + r * a.ldx + base;
@@ -329,10 +343,7 @@ __global__ void __launch_bounds__(NT, 1) sampler_rows_kernel(const SamplerArgs a
         const double us[2] = {u0, u1};
         for (int q = 0; q < 2 && i + q < len; ++q) {
           double g;
-          if (fast)
-            g = GUMBEL ? gumbel_fast(us[q]) : beta_icdf_fast(us[q], a.inv_alpha);
-          else
-            g = GUMBEL ? gumbel_from_u(us[q]) : beta_icdf(us[q], a.inv_alpha);
+          g = GUMBEL ? gumbel_from_u(us[q]) : beta_icdf(us[q], a.inv_alpha);
           top2_add(m1, m2, xr[i + q] + g);
         }
       }

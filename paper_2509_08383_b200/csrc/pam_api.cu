@@ -415,7 +415,7 @@ int sampler_batch_impl(const double* d_x, int64_t ld_x, int64_t B, int64_t n, co
   const int flavour = flavour_of(prm);
   const void* fn = flavour == 2 ? var->stop[gumbel ? 1 : 0] : var->fn[flavour][gumbel ? 1 : 0];
   const int buf_bytes = (int)(((L * 8) + 127) / 128 * 128);
-  const int smem = buf_bytes + (int)sizeof(ControlBlock);
+  const int smem = buf_bytes + kSamplerTabOffset + kSamplerTabBytes;  // + log/exp tables
   const int maxcl = max_active_clusters(fn, var->nt, C, smem);
   if (maxcl <= 0) return cuda_fail(cudaErrorInvalidConfiguration, "no cluster fits (occupancy 0)");
   const int clusters = (int)(B < maxcl ? B : maxcl);

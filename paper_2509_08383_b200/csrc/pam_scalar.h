@@ -19,6 +19,7 @@
 
 #include <stdint.h>
 #include <math.h>
+#include "pam_logexp_tables.h"
 #include <string.h>
 
 #if defined(__CUDACC__)
@@ -272,98 +273,135 @@ PAM_HD double log_p(double x) {
   return fma(ed, LN2_HI, fma(ed, LN2_LO, logm));
 }
 
+// ------------------------------------------- table-driven log / exp -------
+// The sampler evaluates a log and an exp per element for its noise and an exp
+// per element for the nucleus test, so those use table-driven forms (~12 fp64
+// operations each instead of ~25): tables from tools/gen_logexp_tables.py
+// (pam_logexp_tables.h), identical on host and device, mirrored bit for bit
+// by the oracle (orc_log_t / orc_exp_t).  Accuracy <= 2 ulp (tests/test_oracle.py).
+//
+// log_t_core: positive normal x.  x = 2^e m, m in [1, 2); i = top 7 mantissa
+// bits; m/2 and e + 1 for i >= 53, so m in [0.707, 1.414); r = m * invc[i] - 1
+// (|r| < 2^-7, one rounding), log1p(r) to degree 8; invc = 1 on the two
+// intervals next to 1, so results near x = 1 keep their relative accuracy.
+PAM_HD double log_t_core(double x, const double* invc, const double* logc) {
+  const uint64_t xb = pam_double_to_bits(x);
+  const uint64_t mb = xb & 0x000fffffffffffffULL;
+  const int i = (int)(mb >> 45);
+  const bool half = i >= 53;
+  const int e = (int)(xb >> 52) - 1023 + (half ? 1 : 0);
+  double m = pam_bits_to_double(mb | 0x3ff0000000000000ULL);
+  m = half ? m * 0.5 : m;
+  const double r = fma(m, invc[i], -1.0);
+  double a = fma(r, -0.125, 0x1.2492492492492p-3);  // -1/8, 1/7
+  a = fma(a, r, -0x1.5555555555555p-3);             // -1/6
+  a = fma(a, r, 0x1.999999999999ap-3);              // 1/5
+  a = fma(a, r, -0.25);
+  a = fma(a, r, 0x1.5555555555555p-2);              // 1/3
+  a = fma(a, r, -0.5);
+  const double lp = fma(r * r, a, r);
+  const double t = logc[i] + lp;
+  const double ed = (double)e;
+  return fma(ed, 0x1.62e42fefa3800p-1, fma(ed, 0x1.ef35793c76730p-45, t));
+}
+// exp_t_parts: x = (128 q + j) ln2/128 + r (two-step Cody-Waite), |r| <= ln2/256,
+// exp(r) - 1 to degree 5; returns 2^(j/128) (1 + (exp(r) - 1)) with one rounding
+// and the binary exponent q.
+PAM_HD double exp_t_parts(double x, const double* e2, int* q) {
+  const double k = rint(x * 0x1.71547652b82fep+7);  // 128 / ln2
+  double r = fma(-k, PAM_EXPT_LN2N_HI, x);
+  r = fma(-k, PAM_EXPT_LN2N_LO, r);
+  double p = fma(r, 0x1.1111111111111p-7, 0x1.5555555555555p-5);  // 1/120, 1/24
+  p = fma(p, r, 0x1.5555555555555p-3);                              // 1/6
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  const double em1 = r * p;
+  const int ki = (int)k;
+  const double t = e2[ki & 127];
+  *q = ki >> 7;  // arithmetic shift: floor(ki / 128)
+  return fma(t, em1, t);
+}
+// for -708 <= x <= 709 (q in [-1022, 1023]: no subnormal result, no overflow)
+PAM_HD double exp_t_core(double x, const double* e2) {
+  int q;
+  const double y = exp_t_parts(x, e2, &q);
+  return y * pam_pow2(q);
+}
+
+#ifdef __CUDACC__
+__device__ static const double pam_d_logt_invc[128] = {PAM_LOGT_INVC_VALUES};
+__device__ static const double pam_d_logt_logc[128] = {PAM_LOGT_LOGC_VALUES};
+__device__ static const double pam_d_expt_e2[128] = {PAM_EXPT_E2_VALUES};
+#endif
+static const double pam_h_logt_invc[128] = {PAM_LOGT_INVC_VALUES};
+static const double pam_h_logt_logc[128] = {PAM_LOGT_LOGC_VALUES};
+static const double pam_h_expt_e2[128] = {PAM_EXPT_E2_VALUES};
+#ifdef __CUDA_ARCH__
+#define PAM_LOGT_INVC pam_d_logt_invc
+#define PAM_LOGT_LOGC pam_d_logt_logc
+#define PAM_EXPT_E2 pam_d_expt_e2
+#else
+#define PAM_LOGT_INVC pam_h_logt_invc
+#define PAM_LOGT_LOGC pam_h_logt_logc
+#define PAM_EXPT_E2 pam_h_expt_e2
+#endif
+
+// Portable forms with exp_p / log_p's special cases (NaN, range, zero, inf;
+// subnormal log arguments take log_p, which the sampler never produces).
+PAM_HD double exp_t(double x) {
+  if (x != x) return x;
+  if (x > 709.782712893383973096) return HUGE_VAL;
+  if (x < -708.3964185322641) return 0.0;
+  int q;
+  const double y = exp_t_parts(x, PAM_EXPT_E2, &q);
+  if (q < -1021) {  // result may be subnormal: flush (as exp_p)
+    const double t = ldexp(y, q + 60);
+    return (t < 0x1p-962) ? 0.0 : ldexp(t, -60);
+  }
+  if (q > 1023) return (y * pam_pow2(q - 1)) * 2.0;
+  return y * pam_pow2(q);
+}
+PAM_HD double log_t(double x) {
+  if (x != x) return x;
+  if (x < 0.0) return (double)NAN;
+  if (x == 0.0) return -HUGE_VAL;
+  if (x > 1.79769313486231570815e308) return x;  // +inf
+  if ((pam_double_to_bits(x) >> 52) == 0) return log_p(x);  // subnormal
+  return log_t_core(x, PAM_LOGT_INVC, PAM_LOGT_LOGC);
+}
+
 // ------------------------------------------------------- sampling --------
 // Beta(alpha,1) inverse CDF u^(1/alpha), given inv_alpha.
 PAM_HD double beta_icdf(double u, double inv_alpha) {
   if (!(u > 0.0)) return 0.0;
   if (u >= 1.0) return 1.0;
   if (inv_alpha == 1.0) return u;
-  return exp_p(log_p(u) * inv_alpha);
+  return exp_t(log_t(u) * inv_alpha);
 }
 
 // Gumbel from uniform -log(-log u), u in (0,1).
-PAM_HD double gumbel_from_u(double u) { return -log_p(-log_p(u)); }
+PAM_HD double gumbel_from_u(double u) { return -log_t(-log_t(u)); }
 
 #ifdef __CUDACC__
 // ---- branch-free device forms of the above, bit-identical on their domain ----
 // The portable functions branch per element on special cases (NaN, 0, inf,
-// subnormal, overflow) and divide with div.rn.f64, whose slow-path call splits
-// the sampler's unrolled noise loop into one basic block per element (no
-// cross-element ILP).  On the inputs the sampler feeds them, none of the special
-// cases can occur, and these forms run the same arithmetic without branches.
-// tools/fastmath_check.cu compares them bit for bit with the portable forms.
+// subnormal, overflow); on the inputs the sampler feeds them none can occur, so
+// these run the same arithmetic without branches (and with the tables in
+// shared memory).  tools/fastmath_check.cu compares them bit for bit with the
+// portable forms.
 
-// Correctly rounded a / b for b in [1.7, 2.5], |a| < 1: the div.rn.f64 fast
-// path (reciprocal estimate, two Newton steps, one FMA correction) without its
-// exponent-range checks, which cannot trigger on this range.
-__device__ __forceinline__ double pam_div_nr(double a, double b) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
-  double e = fma(-b, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-b, y, 1.0);
-  y = fma(y, e, y);
-  const double q = a * y;
-  const double r = fma(-b, q, a);
-  return fma(r, y, q);
+// Table-driven noise with the tables in shared memory (t = invc[128],
+// logc[128], e2[128]; the sampler copies them there once per CTA): the same
+// arithmetic as beta_icdf / gumbel_from_u on the sampler's domain, u in
+// [2^-53, 1 - 2^-53] and inv_alpha <= 19 (log(u) * inv_alpha >= -700, checked
+// once per launch), so bit-identical to them and to the oracle.
+__device__ __forceinline__ double beta_icdf_tab(double u, double inv_alpha, const double* t) {
+  return inv_alpha == 1.0 ? u : exp_t_core(log_t_core(u, t, t + 128) * inv_alpha, t + 256);
+}
+__device__ __forceinline__ double gumbel_tab(double u, const double* t) {
+  return -log_t_core(-log_t_core(u, t, t + 128), t, t + 128);
 }
 
-// log_p for positive normal finite x.
-__device__ __forceinline__ double pam_log_fast(double x) {
-  const uint64_t xb = pam_double_to_bits(x);
-  int e = (int)(xb >> 52) - 1022;
-  double m = pam_bits_to_double((xb & 0x000fffffffffffffULL) | 0x3fe0000000000000ULL);
-  const bool lo = m < 0x1.6a09e667f3bcdp-1;
-  m = lo ? m + m : m;
-  e = lo ? e - 1 : e;
-  const double f = pam_div_nr(m - 1.0, m + 1.0);
-  const double s = f * f;
-  double q = 0x1.642c8590b2164p-5;
-  q = fma(q, s, 0x1.8618618618618p-5);
-  q = fma(q, s, 0x1.af286bca1af28p-5);
-  q = fma(q, s, 0x1.e1e1e1e1e1e1ep-5);
-  q = fma(q, s, 0x1.1111111111111p-4);
-  q = fma(q, s, 0x1.3b13b13b13b14p-4);
-  q = fma(q, s, 0x1.745d1745d1746p-4);
-  q = fma(q, s, 0x1.c71c71c71c71cp-4);
-  q = fma(q, s, 0x1.2492492492492p-3);
-  q = fma(q, s, 0x1.999999999999ap-3);
-  q = fma(q, s, 0x1.5555555555555p-2);
-  const double t = f + f;
-  const double logm = fma(t * s, q, t);
-  const double ed = (double)e;
-  return fma(ed, 0x1.62e42fefa3800p-1, fma(ed, 0x1.ef35793c76730p-45, logm));
-}
-
-// exp_p for -700 <= x <= 709 (k = rint(x / ln2) in [-1010, 1023]: no flush, no overflow).
-__device__ __forceinline__ double pam_exp_fast(double x) {
-  const double k = rint(x * 0x1.71547652b82fep+0);
-  double r = fma(-k, 0x1.62e42fefa3800p-1, x);
-  r = fma(-k, 0x1.ef35793c76730p-45, r);
-  double p = 0x1.6124613a86d09p-33;
-  p = fma(p, r, 0x1.1eed8eff8d898p-29);
-  p = fma(p, r, 0x1.ae64567f544e4p-26);
-  p = fma(p, r, 0x1.27e4fb7789f5cp-22);
-  p = fma(p, r, 0x1.71de3a556c734p-19);
-  p = fma(p, r, 0x1.a01a01a01a01ap-16);
-  p = fma(p, r, 0x1.a01a01a01a01ap-13);
-  p = fma(p, r, 0x1.6c16c16c16c17p-10);
-  p = fma(p, r, 0x1.1111111111111p-7);
-  p = fma(p, r, 0x1.5555555555555p-5);
-  p = fma(p, r, 0x1.5555555555555p-3);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  return p * pam_pow2((int)k);
-}
-
-// beta_icdf for u in [2^-53, 1 - 2^-53] (u01_from_bits) and inv_alpha <= 19
-// (then log(u) * inv_alpha >= -700); callers check inv_alpha once per launch.
-__device__ __forceinline__ double beta_icdf_fast(double u, double inv_alpha) {
-  return inv_alpha == 1.0 ? u : pam_exp_fast(pam_log_fast(u) * inv_alpha);
-}
-// gumbel_from_u for u in [2^-53, 1 - 2^-53].
-__device__ __forceinline__ double gumbel_fast(double u) { return -pam_log_fast(-pam_log_fast(u)); }
 #endif
 
 }  // namespace pam

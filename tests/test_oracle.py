@@ -352,3 +352,29 @@ def test_cutmax_jvp_oracle(orc, pam):
         assert np.max(np.abs(fd - a)) <= 1e-4 * np.max(np.abs(a)) + 1e-9
     st, _, _ = orc.cutmax_jvp(np.full(8, 2.5), np.ones(8), prm)
     assert st == pam._abi.PAM_ERR_SINGULAR
+
+
+def test_table_log_exp_accuracy(orc):
+    """The sampler's table-driven log / exp (oracle orc_log_t / orc_exp_t, the
+    kernel's pam_scalar.h log_t / exp_t): <= 2 ulp against libm on the
+    sampler's domains (uniforms in (0,1), the Gumbel inner values, Beta
+    exponents in [-700, 0], nucleus exponents x - max <= 0) and beyond."""
+    import numpy as np
+
+    rng = np.random.default_rng(7)
+    us = np.concatenate([rng.random(20000), 1.0 - rng.random(2000) * 1e-12, rng.random(2000) * 1e-300,
+                         np.exp(rng.uniform(-36.7, 0.0, 4000)), rng.uniform(1.0, 1e6, 2000)])
+    for u in us:
+        if u <= 0.0:
+            continue
+        ref = math.log(u)
+        got = orc.scalar("log_t", float(u))
+        assert abs(got - ref) <= 2 * math.ulp(ref) + 1e-300, (u, got, ref)
+    xs = np.concatenate([rng.uniform(-700.0, 0.0, 20000), rng.uniform(-1e-3, 1e-3, 2000),
+                         rng.uniform(0.0, 709.0, 2000)])
+    for x in xs:
+        ref = math.exp(x)
+        got = orc.scalar("exp_t", float(x))
+        assert abs(got - ref) <= 2 * math.ulp(ref), (x, got, ref)
+    assert orc.scalar("exp_t", 0.0) == 1.0 and orc.scalar("log_t", 1.0) == 0.0
+    assert orc.scalar("exp_t", -800.0) == 0.0 and math.isinf(orc.scalar("exp_t", 800.0))

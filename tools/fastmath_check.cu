@@ -1,7 +1,9 @@
 // fastmath_check.cu — bit-for-bit check of the sampler's branch-free device
-// forms (pam_div_nr, pam_log_fast, pam_exp_fast, beta_icdf_fast, gumbel_fast)
-// against the portable functions the oracle mirrors (dev tool; exit 1 on any
-// mismatch).
+// forms with the tables in shared memory (log_t_core, exp_t_core,
+// beta_icdf_tab, gumbel_tab; pam_scalar.h) against the portable forms
+// (log_t, exp_t, beta_icdf, gumbel_from_u) that the host library and the CPU
+// oracle evaluate identically (dev tool; exit 1 on any mismatch).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false -o tools/fastmath_check tools/fastmath_check.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "../paper_2509_08383_b200/csrc/pam_scalar.h"
@@ -19,53 +21,57 @@ __device__ void report(int t, double in, double a, double b) {
   }
 }
 
-__global__ void check(uint64_t seed, int per_thread) {
+__global__ void check(uint64_t seed, int per_thread, double inv_alpha) {
+  __shared__ double tabs[384];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+    tabs[i] = pam_d_logt_invc[i];
+    tabs[128 + i] = pam_d_logt_logc[i];
+    tabs[256 + i] = pam_d_expt_e2[i];
+  }
+  __syncthreads();
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   for (int i = 0; i < per_thread; ++i) {
     const uint64_t r = mix(seed ^ (tid * 0x9e3779b97f4a7c15ULL + i));
     const uint64_t r2 = mix(r + 0x1234567);
-    // 0: division on the log's range: m in [sqrt(1/2), sqrt(2))
-    const double m = 0x1.6a09e667f3bcdp-1 + (double)(r >> 11) * 0x1p-53 * (1.4142135623730951 - 0.7071067811865476);
-    report(0, m, pam_div_nr(m - 1.0, m + 1.0), (m - 1.0) / (m + 1.0));
-    // 1: log on the uniforms
+    // the sampler's uniforms: ((bits >> 12) + 0.5) 2^-52
     const double u = u01_from_bits((uint32_t)r, (uint32_t)(r >> 32));
-    report(1, u, pam_log_fast(u), log_p(u));
-    // 2: log on (1e-16, 40] (gumbel's outer log)
-    const double w = -log_p(u);
-    report(2, w, pam_log_fast(w), log_p(w));
-    // 3: exp on [-700, 709]
-    const double x = -700.0 + (double)(r2 >> 11) * 0x1p-53 * 1409.0;
-    report(3, x, pam_exp_fast(x), exp_p(x));
-    // 4: exp on [-2, 0] (beta noise, x - max near the top)
-    const double x2 = -(double)(r2 >> 11) * 0x1p-52;
-    report(4, x2, pam_exp_fast(x2), exp_p(x2));
-    // 5: beta noise for alpha(0.9), alpha(0.95), 2, 1/19
-    const double ia[4] = {1.0 / 21.854345326782836, 1.0 / 58.40397667459505, 0.5, 19.0};
-    const double inv = ia[(r2 >> 3) & 3];
-    report(5, u, beta_icdf_fast(u, inv), beta_icdf(u, inv));
-    // 6: gumbel noise
-    report(6, u, gumbel_fast(u), gumbel_from_u(u));
+    report(0, u, log_t_core(u, tabs, tabs + 128), log_t(u));
+    // exp on the nucleus / Beta range [-700, 0]
+    const double x = -700.0 * ((double)(r2 >> 11) * 0x1p-53);
+    report(1, x, exp_t_core(x, tabs + 256), exp_t(x));
+    report(2, u, beta_icdf_tab(u, inv_alpha, tabs), beta_icdf(u, inv_alpha));
+    report(3, u, gumbel_tab(u, tabs), gumbel_from_u(u));
+    // Gumbel's inner value -log u in [2^-53, 36.7]
+    const double w = -log_t(u);
+    report(4, w, log_t_core(w, tabs, tabs + 128), log_t(w));
   }
 }
 
 int main() {
-  const int blocks = 148 * 4, threads = 256, per = 512;
-  unsigned long long zero[8] = {0};
-  cudaMemcpyToSymbol(g_bad, zero, sizeof zero);
-  for (int s = 0; s < 4; ++s) check<<<blocks, threads>>>(0x2509083830000ULL + s, per);
-  cudaDeviceSynchronize();
-  unsigned long long bad[8];
-  double first[8][3];
-  cudaMemcpyFromSymbol(bad, g_bad, sizeof bad);
-  cudaMemcpyFromSymbol(first, g_first, sizeof first);
-  const char* nm[7] = {"div (log range)", "log(uniform)", "log(-log u)", "exp[-700,709]", "exp[-2,0]", "beta_icdf", "gumbel"};
-  const double n = 4.0 * blocks * threads * per;
-  int fails = 0;
-  for (int t = 0; t < 7; ++t) {
-    printf("%-16s %.3g samples: %llu mismatches", nm[t], n, bad[t]);
-    if (bad[t]) { printf("  (first: in %.17g fast %.17g ref %.17g)", first[t][0], first[t][1], first[t][2]); ++fails; }
-    printf("\n");
+  const char* names[5] = {"log_t_core(u)", "exp_t_core(x)", "beta_icdf_tab", "gumbel_tab", "log_t_core(-log u)"};
+  const double inv_alphas[3] = {1.0 / 21.854345326782834, 1.0 / 3.0, 19.0};
+  unsigned long long total = 0;
+  int fail = 0;
+  for (int a = 0; a < 3; ++a) {
+    unsigned long long zero[8] = {0};
+    cudaMemcpyToSymbol(g_bad, zero, sizeof zero);
+    const int blocks = 148 * 8, threads = 256, per = 1024;
+    check<<<blocks, threads>>>(0x5eed + a, per, inv_alphas[a]);
+    if (cudaDeviceSynchronize() != cudaSuccess) { std::printf("kernel failed\n"); return 2; }
+    unsigned long long bad[8];
+    double first[8][3];
+    cudaMemcpyFromSymbol(bad, g_bad, sizeof bad);
+    cudaMemcpyFromSymbol(first, g_first, sizeof first);
+    const unsigned long long n = (unsigned long long)blocks * threads * per;
+    total += n;
+    for (int t = 0; t < 5; ++t) {
+      std::printf("inv_alpha %.6f %-20s %llu mismatches in %llu\n", inv_alphas[a], names[t], bad[t], n);
+      if (bad[t]) {
+        fail = 1;
+        std::printf("   first: in %.17g fast %.17g portable %.17g\n", first[t][0], first[t][1], first[t][2]);
+      }
+    }
   }
-  printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
-  return fails ? 1 : 0;
+  std::printf("%s (%llu samples per function)\n", fail ? "MISMATCH" : "all bit-identical", total);
+  return fail;
 }
