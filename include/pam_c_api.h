@@ -179,6 +179,19 @@ int pam_gumbel_sample_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int6
                                 double* d_onehot, int64_t ld_onehot,
                                 int32_t* d_row_status, void* stream);
 
+/* ---- the top-p nucleus itself (csrc/nucleus_set.cu) ---
+ * Per row: cutoff[r] = the smallest logit inside the top-p nucleus of
+ * softmax(x_r) (ties included), size[r] = number of entries >= cutoff, mass[r] =
+ * their softmax mass; x_k is inside <=> x_k >= cutoff[r].  The cumulative-mass
+ * step is a cluster-wide histogram scan (radix select) over 40-bit fixed-point
+ * masses floor(exp(x - max) 2^40 + 1/2), which makes the result independent of
+ * the summation order (bit-exact against the oracle).  n <= 196608.  Outputs
+ * are nullable.  Replaces the nucleus ground truth of sampling.violationExperiment
+ * (SPEC.md:447-455, 464).  Row status: PAM_OK or PAM_ERR_NON_FINITE. */
+int pam_nucleus_set_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int64_t n, double p,
+                              double* d_cutoff, int32_t* d_size, double* d_mass,
+                              int32_t* d_row_status, void* stream);
+
 /* ---- analysis outputs (csrc/analysis_kernel.cuh) -------------------
  * convergenceTrace: d_out[B][T][4] = {mu, s2, U, fraction of
  * entries below the mean} per iteration, U = sum_{j != top} (r_j - rbar)^2 the

@@ -98,6 +98,15 @@ struct SampleOutcome {
   bool tieWarning = false;
 };
 
+/// The top-p nucleus itself (smallest prefix of the descending
+/// softmax with cumulative mass >= p, ties included): entry k is inside <=>
+/// x[k] >= cutoff.  The ground truth of violationExperiment.
+struct NucleusSet {
+  double cutoff = 0.0;
+  int size = 0;
+  double mass = 0.0;
+};
+
 // ---- single-vector API (host vectors; GPU underneath) ----------------------
 ScoreVector cutmax(const LogitVector& x, const CutMaxParams& params);
 std::pair<std::vector<double>, ResidualStats> cutmaxStep(const std::vector<double>& y, int p, double c);
@@ -105,6 +114,7 @@ SampleOutcome nucleusOneShotSample(const LogitVector& x, const SamplerConfig& cf
                                    std::uint64_t row_index = 0);
 SampleOutcome gumbelMaxSample(const LogitVector& x, const CutMaxParams& params, std::uint64_t seed,
                               double nucleus_p = 0.9);
+NucleusSet nucleusSet(const LogitVector& x, double p);
 
 // ---- scalar API ------------------------------------------------------------
 double goldschmidtInv(double x, const ApproxConfig& cfg);

@@ -649,6 +649,70 @@ int orc_nucleus_inside(const double* x, int64_t n, double p, int64_t tok) {
   return above < p * total;
 }
 
+/* The top-p nucleus itself (softmax probabilities sorted descending,
+ * smallest prefix with cumulative mass >= p, ties included), as the
+ * set form of orc_nucleus_inside: v is inside <=> mass strictly above v < p.
+ * Masses are 40-bit fixed-point integers w_i = floor(exp_t(x_i - m) 2^40 + 1/2)
+ * (0 below m - 64), so the sums are exact and order-free and the GPU's histogram
+ * scan (csrc/nucleus_set.cu) reproduces this sort-and-walk bit for bit:
+ *   inside(v) <=> (double)A(v) < p * (double)W,  A(v) = sum of w over {x > v}.
+ * Outputs: cutoff = smallest inside logit, size = entries >= cutoff, mass =
+ * their share of W.  Non-finite input: PAM_ERR_NON_FINITE, NaN / 0 / NaN. */
+typedef struct { double x; uint64_t q; } orc_nw;
+static int orc_nw_desc(const void* a, const void* b) {
+  const double xa = ((const orc_nw*)a)->x, xb = ((const orc_nw*)b)->x;
+  return xa > xb ? -1 : (xa < xb ? 1 : 0);
+}
+int orc_nucleus_set(const double* x, int64_t n, double p, double* cutoff, int32_t* size, double* mass) {
+  int64_t i;
+  *cutoff = NAN; *size = 0; *mass = NAN;
+  if (n < 1) return PAM_ERR_BAD_ARGUMENT;
+  if (!(p > 0.0 && p < 1.0)) return PAM_ERR_DOMAIN;
+  for (i = 0; i < n; ++i) if (!isfinite(x[i])) return PAM_ERR_NON_FINITE;
+  double m = x[0];
+  for (i = 1; i < n; ++i) if (x[i] > m) m = x[i];
+  m = m + 0.0;
+  orc_nw* e = (orc_nw*)malloc((size_t)n * sizeof(orc_nw));
+  if (!e) return PAM_ERR_BAD_ARGUMENT;
+  uint64_t W = 0;
+  for (i = 0; i < n; ++i) {
+    const double xi = x[i] + 0.0;  /* -0 -> +0, as the kernel's key does */
+    const double t = xi - m;
+    e[i].x = xi;
+    e[i].q = t < -64.0 ? 0 : (uint64_t)(orc_exp_t(t) * 0x1p40 + 0.5);
+    W += e[i].q;
+  }
+  qsort(e, (size_t)n, sizeof(orc_nw), orc_nw_desc);
+  const double pW = p * (double)W;
+  uint64_t above = 0, mq = 0;
+  int64_t cnt = 0;
+  i = 0;
+  while (i < n) {
+    int64_t j = i;
+    uint64_t gw = 0;
+    while (j < n && e[j].x == e[i].x) { gw += e[j].q; ++j; }
+    if (e[i].q == 0 || !((double)above < pW)) break;
+    *cutoff = e[i].x;
+    cnt += j - i;
+    mq = above + gw;
+    above += gw;
+    i = j;
+  }
+  *size = (int32_t)cnt;
+  *mass = (double)mq / (double)W;
+  free(e);
+  return PAM_OK;
+}
+int64_t orc_nucleus_set_batch(const double* x, int64_t ld, int64_t B, int64_t n, double p, double* cutoff,
+                              int32_t* size, double* mass, int32_t* status) {
+  int64_t r, bad = 0;
+  for (r = 0; r < B; ++r) {
+    status[r] = orc_nucleus_set(x + r * ld, n, p, &cutoff[r], &size[r], &mass[r]);
+    bad += status[r] != PAM_OK;
+  }
+  return bad;
+}
+
 /* nucleusOneShotSample (Alg. 3) and, with
  * gumbel != 0, gumbelMaxSample. */
 int orc_sample(const double* x, int64_t n, const pam_sampler_cfg* cfg, const pam_cutmax_params* prm,

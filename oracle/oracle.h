@@ -88,6 +88,9 @@ int orc_tie_warning(const double* x, int64_t n);
 
 /* sampling */
 int orc_nucleus_inside(const double* x, int64_t n, double p, int64_t tok);
+int orc_nucleus_set(const double* x, int64_t n, double p, double* cutoff, int32_t* size, double* mass);
+int64_t orc_nucleus_set_batch(const double* x, int64_t ld, int64_t B, int64_t n, double p, double* cutoff,
+                              int32_t* size, double* mass, int32_t* status);
 int orc_sample(const double* x, int64_t n, const pam_sampler_cfg* cfg, const pam_cutmax_params* prm,
                uint64_t row, int gumbel, int32_t* token, uint8_t* inside, double* onehot);
 int64_t orc_sample_batch(const double* x, int64_t ld, int64_t B, int64_t n, const pam_sampler_cfg* cfg,

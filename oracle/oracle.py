@@ -104,6 +104,7 @@ _SIG = {
     "orc_cutmax_jvp": (C.c_int, [_P, _P, _I64, _PRM, _P, _P]),
     "orc_tie_warning": (C.c_int, [_P, _I64]),
     "orc_nucleus_inside": (C.c_int, [_P, _I64, C.c_double, _I64]),
+    "orc_nucleus_set_batch": (C.c_int64, [_P, _I64, _I64, _I64, C.c_double, _P, _P, _P, _P]),
     "orc_sample": (C.c_int, [_P, _I64, C.POINTER(_abi.pam_sampler_cfg), _PRM, C.c_uint64, C.c_int, _P, _P, _P]),
     "orc_sample_batch": (C.c_int64, [_P, _I64, _I64, _I64, C.POINTER(_abi.pam_sampler_cfg), _PRM, C.c_int, _P, _P,
                                      _P, C.c_int]),
@@ -180,6 +181,20 @@ def sample_batch(X, cfg: _abi.pam_sampler_cfg, prm, gumbel: bool = False, nthrea
 def nucleus_inside(x, p: float, tok: int) -> bool:
     x = _f64(x)
     return bool(load().orc_nucleus_inside(x.ctypes.data, x.shape[0], p, tok))
+
+
+def nucleus_set_batch(X, p: float):
+    """Top-p nucleus of every row -> (cutoff, size, mass, status)."""
+    lib = load()
+    X = _f64(X)
+    if X.ndim == 1:
+        X = X[None, :]
+    B, n = X.shape
+    cut, mass = np.empty(B), np.empty(B)
+    size, st = np.empty(B, dtype=np.int32), np.empty(B, dtype=np.int32)
+    lib.orc_nucleus_set_batch(X.ctypes.data, n, B, n, float(p), cut.ctypes.data, size.ctypes.data, mass.ctypes.data,
+                              st.ctypes.data)
+    return cut, size, mass, st
 
 
 def cutmax_step(y, p: int, c: float, eps_var: float = 1e-24):

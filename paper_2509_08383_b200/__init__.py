@@ -10,7 +10,7 @@ from .polyargmax import (ApproxConfig, CutMaxParams, ResidualStats, SampleOutcom
                          kernel_launch_count, launch_info, nucleus_sample_batch_device, nucleusAlpha,
                          nucleusOneShotSample, uniform, violationExperiment, ingest, ingest_pinned, write_lgt1,
                          convergence_trace_batch_device, convergenceTrace, cutmax_jvp_batch_device, cutmaxJvp,
-                         cutmaxJacobian, geometry_override, general_p3_kernel)
+                         cutmaxJacobian, geometry_override, general_p3_kernel, nucleus_set_batch_device, nucleusSet)
 
 __all__ = [
     "ApproxConfig", "CutMaxParams", "ResidualStats", "SampleOutcome", "SamplerConfig", "ScoreVector",
@@ -19,5 +19,5 @@ __all__ = [
     "kernel_launch_count", "launch_info", "nucleus_sample_batch_device", "nucleusAlpha", "nucleusOneShotSample",
     "uniform", "violationExperiment", "ingest", "ingest_pinned", "write_lgt1", "convergence_trace_batch_device", "convergenceTrace",
     "cutmax_jvp_batch_device", "cutmaxJvp", "cutmaxJacobian", "Error", "FormatError", "SingularityError", "DegenerateInputError", "InvalidParamsError", "RangeError", "DomainError",
-    "NonFiniteError", "CudaError", "TieWarning", "geometry_override", "general_p3_kernel",
+    "NonFiniteError", "CudaError", "TieWarning", "geometry_override", "general_p3_kernel", "nucleus_set_batch_device", "nucleusSet",
 ]

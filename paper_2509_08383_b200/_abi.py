@@ -98,6 +98,7 @@ SIGNATURES = {
                                                C.POINTER(pam_cutmax_params), _P, _P, _P, _I64, _P, _P]),
     "pam_gumbel_sample_batch_f64": (C.c_int, [_P, _I64, _I64, _I64, C.POINTER(pam_sampler_cfg),
                                               C.POINTER(pam_cutmax_params), _P, _P, _P, _I64, _P, _P]),
+    "pam_nucleus_set_batch_f64": (C.c_int, [_P, _I64, _I64, _I64, C.c_double, _P, _P, _P, _P, _P]),
     "pam_query_launch": (C.c_int, [C.c_int, _I64, _I64, C.POINTER(pam_cutmax_params), C.POINTER(pam_launch_info)]),
     "pam_kernel_launch_count": (C.c_int64, []),
     "pam_last_cuda_error": (C.c_char_p, []),

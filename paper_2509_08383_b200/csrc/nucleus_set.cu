@@ -1,0 +1,340 @@
+// nucleus_set.cu — the top-p nucleus itself (cutoff logit, size, mass) by a
+// cluster-wide radix select: the cumulative-mass step of SPEC.md:464 ("softmax
+// probabilities sorted descending, smallest prefix with cumulative mass >= p,
+// ties included"; top-p definition) as a histogram + scan over a
+// thread-block cluster, with no sort.  SURVEY.md §8 row a11 (the full cutoff /
+// nucleus size form of the membership test fused into nucleus_kernel.cuh).
+//
+// Definition (restated in oracle.c orc_nucleus_set, which sorts):
+//   m   = max x;  w_i = floor(exp_t(x_i - m) * 2^40 + 1/2)  (0 when x_i < m - 64):
+//         the softmax masses as 40-bit fixed-point integers, so every sum below
+//         is an exact integer and does not depend on the order of summation;
+//   W   = sum w_i;  A(v) = sum of w_k over {x_k > v};
+//   v is inside the nucleus  <=>  (double)A(v) < p * (double)W   (ties share A);
+//   cutoff = the smallest inside value, size = #{x_i >= cutoff, w_i > 0},
+//   mass = (A(cutoff) + weight of the entries equal to cutoff) / W.
+// inside() is monotone in v, so the cutoff is found by descending the bits of
+// an order-preserving 64-bit key of x, 8 bits per level: each CTA histograms
+// the weights and counts of its slice's candidates (warp-aggregated shared
+// atomics: match.any + REDUX), the cluster's histograms are summed through
+// distributed shared memory, and one warp scans the 256 buckets from the top for
+// the lowest non-empty bucket whose entries can still be inside.  Integer
+// arithmetic throughout: every CTA takes the same decision, and the result is
+// bit-identical to the oracle's.
+//
+// One row per cluster (C = 1..16 CTAs, slice keys and weights resident in
+// shared memory: 16 bytes per element), rows strided over the persistent
+// clusters.  HBM traffic: 8n bytes read per row, 24 bytes written.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "../../include/pam_c_api.h"
+#include "pam_ptx.cuh"
+#include "pam_scalar.h"
+
+extern "C" void pam_internal_count_launch(void);   // pam_api.cu: kernel_launch_count()
+extern "C" int pam_internal_cuda_fail(int e, const char* what);
+
+namespace pam {
+namespace {
+
+typedef unsigned long long u64;
+constexpr int kNT = 512;
+constexpr int kLcap = 12288;  // elements per CTA: 2 x 96 KB of shared memory
+constexpr int kWBits = 40;
+
+struct NucSetArgs {
+  const double* x;
+  int64_t ldx, B, n;
+  int32_t L;
+  double p;
+  double* cutoff;
+  int32_t* size;
+  double* mass;
+  int32_t* status;
+};
+
+struct NucSetCtl {
+  u64 hw[2][256];       // weight histogram of the level, double-buffered by level parity
+  uint32_t hc[2][256];  // count histogram
+  u64 tw[256];          // cluster totals of the current level
+  uint32_t tc[256];
+  u64 pmax;             // this CTA's max key / total weight / non-finite flag
+  u64 pw;
+  uint32_t pbad;
+  int sel_b;            // the scan's decision
+  u64 sel_above, sel_w;
+  uint32_t sel_cabove, sel_c;
+};
+
+__device__ __forceinline__ u64 key_of(double x) {
+  const u64 b = (u64)__double_as_longlong(x + 0.0);  // -0 -> +0
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double value_of(u64 k) {
+  const u64 b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+__device__ __forceinline__ u64 ld_dsmem_u64(const void* local, uint32_t rank) {
+  u64 v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ptx::mapa(ptx::smem_addr(local), rank)) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_dsmem_u32(const void* local, uint32_t rank) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ptx::mapa(ptx::smem_addr(local), rank)) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* key = reinterpret_cast<u64*>(smem_raw);
+  u64* qw = key + kLcap;
+  NucSetCtl* c = reinterpret_cast<NucSetCtl*>(qw + kLcap);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const uint32_t C = ptx::cluster_nctarank();
+  const int64_t cid = ptx::cluster_id_x();
+  const int64_t ncl = ptx::nclusters_x();
+  const int64_t base = (int64_t)rank * a.L;
+  const int64_t rem = a.n - base;
+  const int len = rem <= 0 ? 0 : (rem < a.L ? (int)rem : a.L);
+
+  for (int64_t row = cid; row < a.B; row += ncl) {
+    if (tid == 0) {
+      c->pmax = 0;
+      c->pw = 0;
+      c->pbad = 0;
+    }
+    __syncthreads();
+    // ---- keys, row maximum, non-finite check ---------------------------------
+    {
+      const double* xr = a.x + row * a.ldx + base;
+      u64 kmx = 0;
+      uint32_t bad = 0;
+      for (int i = tid; i < len; i += kNT) {
+        const double x = __ldcs(xr + i);
+        bad |= !isfinite(x);
+        const u64 k = key_of(x);
+        key[i] = k;
+        kmx = k > kmx ? k : kmx;
+      }
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) {
+        const u64 o = __shfl_xor_sync(0xffffffffu, kmx, m);
+        kmx = o > kmx ? o : kmx;
+      }
+      bad = __any_sync(0xffffffffu, bad);
+      if (lane == 0) {
+        atomicMax(&c->pmax, kmx);
+        if (bad) atomicOr(&c->pbad, 1u);
+      }
+    }
+    ptx::cluster_sync();  // every CTA's partials are visible cluster-wide
+    u64 kmax = 0;
+    uint32_t bad = 0;
+    for (uint32_t r = 0; r < C; ++r) {
+      const u64 o = ld_dsmem_u64(&c->pmax, r);
+      kmax = o > kmax ? o : kmax;
+      bad |= ld_dsmem_u32(&c->pbad, r);
+    }
+    if (bad) {  // cluster-uniform
+      if (rank == 0 && tid == 0) {
+        if (a.cutoff) a.cutoff[row] = (double)NAN;
+        if (a.size) a.size[row] = 0;
+        if (a.mass) a.mass[row] = (double)NAN;
+        if (a.status) a.status[row] = PAM_ERR_NON_FINITE;
+      }
+      ptx::cluster_sync();  // nobody resets its partials while a peer still reads them
+      continue;
+    }
+    // ---- fixed-point softmax masses and their total ----------------------------
+    const double mx = value_of(kmax);
+    {
+      u64 ws = 0;
+      for (int i = tid; i < len; i += kNT) {
+        const double t = value_of(key[i]) - mx;
+        const u64 q = t < -64.0 ? 0ull : (u64)(exp_t(t) * 0x1p40 + 0.5);
+        qw[i] = q;
+        ws += q;
+      }
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, m);
+      if (lane == 0) atomicAdd(&c->pw, ws);
+    }
+    ptx::cluster_sync();
+    u64 W = 0;
+    for (uint32_t r = 0; r < C; ++r) W += ld_dsmem_u64(&c->pw, r);
+    const double pW = a.p * (double)W;
+
+    // ---- radix descent: 8 levels of 8 key bits ---------------------------------
+    u64 prefix = 0, above = 0;  // above = A(everything in the current bucket's range)
+    uint32_t cabove = 0;
+    u64 eq_w = 0;
+    uint32_t eq_c = 0;
+    for (int lvl = 0; lvl < 8; ++lvl) {
+      const int shift = 56 - 8 * lvl;
+      u64* hw = c->hw[lvl & 1];
+      uint32_t* hc = c->hc[lvl & 1];
+      for (int b = tid; b < 256; b += kNT) {
+        hw[b] = 0;
+        hc[b] = 0;
+      }
+      __syncthreads();
+      for (int i0 = 0; i0 < len; i0 += kNT) {
+        const int i = i0 + tid;
+        u64 k = 0, q = 0;
+        if (i < len) {
+          k = key[i];
+          q = qw[i];
+        }
+        const bool cand = q > 0 && (lvl == 0 || (k >> (shift + 8)) == prefix);
+        const uint32_t cm = __ballot_sync(0xffffffffu, cand);
+        if (cand) {
+          const uint32_t d = (uint32_t)(k >> shift) & 255u;
+          const uint32_t g = __match_any_sync(cm, d);  // lanes of this warp with the same digit
+          const uint32_t lo = __reduce_add_sync(g, (uint32_t)(q & 0xfffffu));
+          const uint32_t hi = __reduce_add_sync(g, (uint32_t)(q >> 20));
+          if (lane == __ffs(g) - 1) {
+            atomicAdd(&hw[d], ((u64)hi << 20) + lo);
+            atomicAdd(&hc[d], (uint32_t)__popc(g));
+          }
+        }
+      }
+      ptx::cluster_sync();  // the cluster's histograms of this level are complete
+      if (tid < 256) {
+        u64 w = 0;
+        uint32_t n_ = 0;
+        for (uint32_t r = 0; r < C; ++r) {
+          w += ld_dsmem_u64(&hw[tid], r);
+          n_ += ld_dsmem_u32(&hc[tid], r);
+        }
+        c->tw[tid] = w;
+        c->tc[tid] = n_;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        // lane l owns buckets 8l .. 8l+7; suffix sums over the lanes above it
+        u64 sw = 0;
+        uint32_t sc = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          sw += c->tw[8 * lane + j];
+          sc += c->tc[8 * lane + j];
+        }
+        u64 aw = sw;  // inclusive suffix scan (lanes >= l)
+        uint32_t ac = sc;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+          const u64 ow = __shfl_down_sync(0xffffffffu, aw, m);
+          const uint32_t oc = __shfl_down_sync(0xffffffffu, ac, m);
+          if (lane + m < 32) {
+            aw += ow;
+            ac += oc;
+          }
+        }
+        u64 rw = above + (aw - sw);  // weight strictly above this lane's top bucket
+        uint32_t rc = cabove + (ac - sc);
+        int best = 256;
+        u64 best_rw = 0;
+        uint32_t best_rc = 0;
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+          const int b = 8 * lane + j;
+          const u64 w = c->tw[b];
+          const uint32_t n_ = c->tc[b];
+          if (n_ > 0 && (double)rw < pW) {  // the bucket's largest entry is inside
+            best = b;
+            best_rw = rw;
+            best_rc = rc;
+          }
+          rw += w;
+          rc += n_;
+        }
+        const int sel = (int)__reduce_min_sync(0xffffffffu, (unsigned)best);
+        if (best == sel && sel < 256) {
+          c->sel_b = sel;
+          c->sel_above = best_rw;
+          c->sel_cabove = best_rc;
+          c->sel_w = c->tw[sel];
+          c->sel_c = c->tc[sel];
+        }
+      }
+      __syncthreads();
+      prefix = (prefix << 8) | (u64)(uint32_t)c->sel_b;
+      above = c->sel_above;
+      cabove = c->sel_cabove;
+      eq_w = c->sel_w;
+      eq_c = c->sel_c;
+      // (the next level zeroes the other histogram buffer: a peer that still reads
+      //  this level's has not reached the next cluster barrier)
+    }
+    if (rank == 0 && tid == 0) {
+      if (a.cutoff) a.cutoff[row] = value_of(prefix);
+      if (a.size) a.size[row] = (int32_t)(cabove + eq_c);
+      if (a.mass) a.mass[row] = (double)(above + eq_w) / (double)W;
+      if (a.status) a.status[row] = PAM_OK;
+    }
+    ptx::cluster_sync();  // partials and histograms are reset only after every peer is done
+  }
+}
+
+}  // namespace
+}  // namespace pam
+
+extern "C" int pam_nucleus_set_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int64_t n, double p,
+                                         double* d_cutoff, int32_t* d_size, double* d_mass, int32_t* d_row_status,
+                                         void* stream) {
+  using namespace pam;
+  if (B < 0 || n < 1 || ld_x < n || (B > 0 && !d_x)) return PAM_ERR_BAD_ARGUMENT;
+  if (!(p > 0.0 && p < 1.0)) return PAM_ERR_DOMAIN;
+  if (B == 0) return PAM_OK;
+  if (n > (int64_t)16 * kLcap) return PAM_ERR_UNSUPPORTED;  // 196608 entries per row
+  int C = 1;
+  while ((int64_t)C * kLcap < n) C *= 2;
+  NucSetArgs ka;
+  ka.x = d_x;
+  ka.ldx = ld_x;
+  ka.B = B;
+  ka.n = n;
+  ka.L = (int32_t)((n + C - 1) / C);
+  ka.p = p;
+  ka.cutoff = d_cutoff;
+  ka.size = d_size;
+  ka.mass = d_mass;
+  ka.status = d_row_status;
+  const int smem = 2 * kLcap * 8 + (int)sizeof(NucSetCtl);
+  const void* fn = (const void*)nucleus_set_kernel;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return pam_internal_cuda_fail((int)e, "cudaFuncSetAttribute(nucleus set smem)");
+  if (C > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return pam_internal_cuda_fail((int)e, "cudaFuncSetAttribute(nucleus set cluster)");
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kNT);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = (cudaStream_t)stream;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)C);
+  int maxcl = 0;
+  e = cudaOccupancyMaxActiveClusters(&maxcl, fn, &cfg);
+  if (e != cudaSuccess || maxcl <= 0)
+    return pam_internal_cuda_fail((int)(e != cudaSuccess ? e : cudaErrorInvalidConfiguration),
+                                  "cudaOccupancyMaxActiveClusters(nucleus set)");
+  const int64_t clusters = B < maxcl ? B : maxcl;
+  cfg.gridDim = dim3((unsigned)(clusters * C));
+  void* args[] = {&ka};
+  e = cudaLaunchKernelExC(&cfg, fn, args);
+  if (e != cudaSuccess) return pam_internal_cuda_fail((int)e, "cudaLaunchKernelExC(nucleus set)");
+  pam_internal_count_launch();
+  return PAM_OK;
+}

@@ -823,6 +823,12 @@ int pam_set_host_chunk_bytes(int64_t bytes) {
 
 int64_t pam_kernel_launch_count(void) { return g_launches.load(); }
 
+// for the entry points that live in their own translation unit (nucleus_set.cu)
+extern "C" __attribute__((visibility("hidden"))) void pam_internal_count_launch(void) { g_launches.fetch_add(1); }
+extern "C" __attribute__((visibility("hidden"))) int pam_internal_cuda_fail(int e, const char* what) {
+  return cuda_fail((cudaError_t)e, what);
+}
+
 void pam_set_trace_buffer(long long* d_buf, int64_t entries) {
   g_trace = d_buf;
   g_trace_entries = d_buf ? entries : 0;

@@ -298,6 +298,24 @@ SampleOutcome gumbelMaxSample(const LogitVector& x, const CutMaxParams& params, 
   return sample_one(x, c, params, true, 0);
 }
 
+NucleusSet nucleusSet(const LogitVector& x, double p) {
+  const std::size_t n = x.size();
+  DeviceBuffer dx(n * 8), dcut(8), dmass(8), dsize(4), dst(4);
+  check_cuda(cudaMemcpy(dx.p, x.data(), n * 8, cudaMemcpyHostToDevice), "H2D");
+  throw_status(pam_nucleus_set_batch_f64((const double*)dx.p, (int64_t)n, 1, (int64_t)n, p, (double*)dcut.p,
+                                         (int32_t*)dsize.p, (double*)dmass.p, (int32_t*)dst.p, nullptr),
+               0);
+  NucleusSet out;
+  std::int32_t st = 0, size = 0;
+  check_cuda(cudaMemcpy(&st, dst.p, 4, cudaMemcpyDeviceToHost), "D2H");
+  throw_status(st, 0);
+  check_cuda(cudaMemcpy(&out.cutoff, dcut.p, 8, cudaMemcpyDeviceToHost), "D2H");
+  check_cuda(cudaMemcpy(&out.mass, dmass.p, 8, cudaMemcpyDeviceToHost), "D2H");
+  check_cuda(cudaMemcpy(&size, dsize.p, 4, cudaMemcpyDeviceToHost), "D2H");
+  out.size = size;
+  return out;
+}
+
 double goldschmidtInv(double x, const ApproxConfig& cfg) {
   const pam_approx_config c = lower_approx(cfg);
   double out = 0.0;

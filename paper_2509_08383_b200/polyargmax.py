@@ -397,6 +397,39 @@ def gumbelMaxSample(x, params: Optional[CutMaxParams] = None, seed: int = 0, nuc
                            params or CutMaxParams(), 0)
 
 
+# ---- the top-p nucleus itself (csrc/nucleus_set.cu) ----------------------
+def nucleus_set_batch_device(x, p: float, stream=None):
+    """Top-p nucleus of softmax(x_r) for CUDA rows (ties included): returns
+    (cutoff [B] float64, size [B] int32, mass [B] float64, status [B] int32);
+    entry k of row r is inside <=> x[r, k] >= cutoff[r].  Cluster histogram scan
+    over fixed-point masses, so the result does not depend on the summation order."""
+    torch = _torch()
+    if x.dim() != 2 or not x.is_cuda or x.dtype != torch.float64:
+        raise InvalidParamsError("x must be a 2-D float64 CUDA tensor")
+    if x.stride(1) != 1:
+        raise InvalidParamsError("rows must be contiguous")
+    B, n = x.shape
+    cutoff = torch.empty(B, dtype=torch.float64, device=x.device)
+    mass = torch.empty(B, dtype=torch.float64, device=x.device)
+    size = torch.empty(B, dtype=torch.int32, device=x.device)
+    status = torch.empty(B, dtype=torch.int32, device=x.device)
+    with torch.cuda.device(x.device):
+        rc = _lib.pam_nucleus_set_batch_f64(x.data_ptr(), x.stride(0), B, n, float(p), cutoff.data_ptr(),
+                                            size.data_ptr(), mass.data_ptr(), status.data_ptr(),
+                                            _stream_ptr(stream, x.device))
+    raise_for_status(rc, what="nucleus_set_batch_device")
+    return cutoff, size, mass, status
+
+
+def nucleusSet(x, p: float):
+    """The top-p nucleus of one logit vector: dict(cutoff, size, mass)."""
+    torch = _torch()
+    xv = torch.as_tensor(np.asarray(x, dtype=np.float64), device="cuda")[None, :]
+    cut, size, mass, st = nucleus_set_batch_device(xv, p)
+    raise_for_status(int(st.item()), row=0)
+    return dict(cutoff=float(cut.item()), size=int(size.item()), mass=float(mass.item()))
+
+
 # ---- analysis (SURVEY §8f; csrc/analysis_kernel.cuh) ---------------------------------
 def convergence_trace_batch_device(x, params: Optional[CutMaxParams] = None, stream=None):
     """convergenceTrace for CUDA rows: returns (out [B, T, 4] = {mu, s2, U,

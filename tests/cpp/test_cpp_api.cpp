@@ -161,6 +161,15 @@ static void test_samplers() {
   uint8_t ins = 0;
   orc_sample(x.data(), (int64_t)x.size(), &sc, &cp, 0, 1, &tok, &ins, nullptr);
   CHECK(g.tokenIndex == tok, "gumbel token %d vs %d", g.tokenIndex, tok);
+  // the nucleus itself: bit-exact against the oracle's sort-and-walk
+  for (double p : {0.9, 0.95}) {
+    const pa::NucleusSet ns = pa::nucleusSet(x, p);
+    double cut = 0, mass = 0;
+    int32_t size = 0;
+    orc_nucleus_set(x.data(), (int64_t)x.size(), p, &cut, &size, &mass);
+    CHECK(ns.cutoff == cut && ns.size == size && ns.mass == mass, "nucleusSet p=%.2f size %d vs %d", p, ns.size, size);
+  }
+  CHECK(throws<pa::DomainError>([&] { pa::nucleusSet(x, 1.5); }), "nucleusSet p > 1");
 }
 
 static void test_scalars() {
