@@ -15,8 +15,8 @@
 //   mass = (A(cutoff) + weight of the entries equal to cutoff) / W.
 // inside() is monotone in v, so the cutoff is found by descending the bits of
 // an order-preserving 64-bit key of x, 8 bits per level: each CTA histograms
-// the weights and counts of its slice's candidates (warp-aggregated shared
-// atomics: match.any + REDUX), the cluster's histograms are summed through
+// the weights and counts of its slice's candidates (shared atomics; the two most
+// common digits of each warp step are pre-summed with REDUX), the cluster's histograms are summed through
 // distributed shared memory, and one warp scans the 256 buckets from the top for
 // the lowest non-empty bucket whose entries can still be inside.  Integer
 // arithmetic throughout: every CTA takes the same decision, and the result is
@@ -53,13 +53,23 @@ struct NucSetArgs {
   int32_t* size;
   double* mass;
   int32_t* status;
+  long long* dbg;  // dev: phase clocks of cluster 0 / CTA 0's first row (pam_dev_nucleus_set_clocks)
 };
 
+#define NS_STAMP(k)                                                        \
+  do {                                                                     \
+    if (a.dbg && blockIdx.x == 0 && tid == 0 && row == cid) a.dbg[k] = clock64(); \
+  } while (0)
+
 struct NucSetCtl {
-  u64 hw[2][256];       // weight histogram of the level, double-buffered by level parity
+  // weight histogram of the level in three 14-bit pieces (native 32-bit shared
+  // atomics; a 64-bit shared add is a CAS loop), double-buffered by level parity
+  uint32_t hp[2][3][256];
   uint32_t hc[2][256];  // count histogram
   u64 tw[256];          // cluster totals of the current level
   uint32_t tc[256];
+  u64 tw2[256];         // (second half of the gather)
+  uint32_t tc2[256];
   u64 pmax;             // this CTA's max key / total weight / non-finite flag
   u64 pw;
   uint32_t pbad;
@@ -78,12 +88,12 @@ __device__ __forceinline__ double value_of(u64 k) {
 }
 __device__ __forceinline__ u64 ld_dsmem_u64(const void* local, uint32_t rank) {
   u64 v;
-  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ptx::mapa(ptx::smem_addr(local), rank)) : "memory");
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ptx::mapa(ptx::smem_addr(local), rank)));
   return v;
 }
 __device__ __forceinline__ uint32_t ld_dsmem_u32(const void* local, uint32_t rank) {
   uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ptx::mapa(ptx::smem_addr(local), rank)) : "memory");
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ptx::mapa(ptx::smem_addr(local), rank)));
   return v;
 }
 
@@ -109,6 +119,7 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
       c->pbad = 0;
     }
     __syncthreads();
+    NS_STAMP(0);
     // ---- keys, row maximum, non-finite check ---------------------------------
     {
       const double* xr = a.x + row * a.ldx + base;
@@ -132,14 +143,18 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
         if (bad) atomicOr(&c->pbad, 1u);
       }
     }
+    NS_STAMP(1);
     ptx::cluster_sync();  // every CTA's partials are visible cluster-wide
-    u64 kmax = 0;
-    uint32_t bad = 0;
-    for (uint32_t r = 0; r < C; ++r) {
-      const u64 o = ld_dsmem_u64(&c->pmax, r);
+    NS_STAMP(2);
+    // lane r reads CTA r's partials (one DSMEM round trip), every warp combines them
+    u64 kmax = lane < (int)C ? ld_dsmem_u64(&c->pmax, (uint32_t)lane) : 0ull;
+    uint32_t bad = lane < (int)C ? ld_dsmem_u32(&c->pbad, (uint32_t)lane) : 0u;
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) {
+      const u64 o = __shfl_xor_sync(0xffffffffu, kmax, m);
       kmax = o > kmax ? o : kmax;
-      bad |= ld_dsmem_u32(&c->pbad, r);
     }
+    bad = __any_sync(0xffffffffu, bad);
     if (bad) {  // cluster-uniform
       if (rank == 0 && tid == 0) {
         if (a.cutoff) a.cutoff[row] = (double)NAN;
@@ -154,9 +169,12 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
     const double mx = value_of(kmax);
     {
       u64 ws = 0;
+#pragma unroll 4
       for (int i = tid; i < len; i += kNT) {
         const double t = value_of(key[i]) - mx;
-        const u64 q = t < -64.0 ? 0ull : (u64)(exp_t(t) * 0x1p40 + 0.5);
+        // exp_t_core = exp_t on [-708, 709] (no special case can occur on [-64, 0])
+        const double e = exp_t_core(t < -64.0 ? -64.0 : t, PAM_EXPT_E2);
+        const u64 q = t < -64.0 ? 0ull : (u64)(e * 0x1p40 + 0.5);
         qw[i] = q;
         ws += q;
       }
@@ -164,9 +182,12 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
       for (int m = 16; m > 0; m >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, m);
       if (lane == 0) atomicAdd(&c->pw, ws);
     }
+    NS_STAMP(3);
     ptx::cluster_sync();
-    u64 W = 0;
-    for (uint32_t r = 0; r < C; ++r) W += ld_dsmem_u64(&c->pw, r);
+    NS_STAMP(4);
+    u64 W = lane < (int)C ? ld_dsmem_u64(&c->pw, (uint32_t)lane) : 0ull;
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) W += __shfl_xor_sync(0xffffffffu, W, m);
     const double pW = a.p * (double)W;
 
     // ---- radix descent: 8 levels of 8 key bits ---------------------------------
@@ -176,13 +197,18 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
     uint32_t eq_c = 0;
     for (int lvl = 0; lvl < 8; ++lvl) {
       const int shift = 56 - 8 * lvl;
-      u64* hw = c->hw[lvl & 1];
+      uint32_t* h0 = c->hp[lvl & 1][0];
+      uint32_t* h1 = c->hp[lvl & 1][1];
+      uint32_t* h2 = c->hp[lvl & 1][2];
       uint32_t* hc = c->hc[lvl & 1];
       for (int b = tid; b < 256; b += kNT) {
-        hw[b] = 0;
+        h0[b] = 0;
+        h1[b] = 0;
+        h2[b] = 0;
         hc[b] = 0;
       }
       __syncthreads();
+#pragma unroll 2
       for (int i0 = 0; i0 < len; i0 += kNT) {
         const int i = i0 + tid;
         u64 k = 0, q = 0;
@@ -192,29 +218,85 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
         }
         const bool cand = q > 0 && (lvl == 0 || (k >> (shift + 8)) == prefix);
         const uint32_t cm = __ballot_sync(0xffffffffu, cand);
-        if (cand) {
-          const uint32_t d = (uint32_t)(k >> shift) & 255u;
-          const uint32_t g = __match_any_sync(cm, d);  // lanes of this warp with the same digit
-          const uint32_t lo = __reduce_add_sync(g, (uint32_t)(q & 0xfffffu));
-          const uint32_t hi = __reduce_add_sync(g, (uint32_t)(q >> 20));
-          if (lane == __ffs(g) - 1) {
-            atomicAdd(&hw[d], ((u64)hi << 20) + lo);
-            atomicAdd(&hc[d], (uint32_t)__popc(g));
+        if (cm == 0u) continue;  // warp-uniform
+        const uint32_t d = (uint32_t)(k >> shift) & 255u;
+        // few distinct digits in the warp (the exponent levels, tie groups): one
+        // REDUX pair and one atomic per digit; many: the buckets are spread and
+        // direct atomics do not contend (a REDUX per distinct digit would serialise)
+        const uint32_t d0 = __shfl_sync(0xffffffffu, d, __ffs(cm) - 1);
+        const uint32_t m0 = __ballot_sync(0xffffffffu, cand && d == d0);
+        const uint32_t rest = cm & ~m0;
+        uint32_t m1 = 0u, d1 = 0u;
+        if (rest) {
+          d1 = __shfl_sync(0xffffffffu, d, __ffs(rest) - 1);
+          m1 = __ballot_sync(0xffffffffu, cand && d == d1);
+        }
+        // q < 2^41 in three 14-bit pieces: a CTA's bucket sums stay below 2^32
+        const uint32_t q0 = (uint32_t)q & 0x3fffu, q1 = (uint32_t)(q >> 14) & 0x3fffu, q2 = (uint32_t)(q >> 28);
+        {
+          const bool in0 = (m0 >> lane) & 1u;
+          const uint32_t s0 = __reduce_add_sync(0xffffffffu, in0 ? q0 : 0u);
+          const uint32_t s1 = __reduce_add_sync(0xffffffffu, in0 ? q1 : 0u);
+          const uint32_t s2 = __reduce_add_sync(0xffffffffu, in0 ? q2 : 0u);
+          if (lane == 0) {
+            atomicAdd(&h0[d0], s0);
+            atomicAdd(&h1[d0], s1);
+            atomicAdd(&h2[d0], s2);
+            atomicAdd(&hc[d0], (uint32_t)__popc(m0));
           }
         }
+        if (m1) {  // warp-uniform
+          const bool in1 = (m1 >> lane) & 1u;
+          const uint32_t s0 = __reduce_add_sync(0xffffffffu, in1 ? q0 : 0u);
+          const uint32_t s1 = __reduce_add_sync(0xffffffffu, in1 ? q1 : 0u);
+          const uint32_t s2 = __reduce_add_sync(0xffffffffu, in1 ? q2 : 0u);
+          if (lane == 0) {
+            atomicAdd(&h0[d1], s0);
+            atomicAdd(&h1[d1], s1);
+            atomicAdd(&h2[d1], s2);
+            atomicAdd(&hc[d1], (uint32_t)__popc(m1));
+          }
+        }
+        if (cand && !(((m0 | m1) >> lane) & 1u)) {  // the remaining digits: direct
+          atomicAdd(&h0[d], q0);
+          atomicAdd(&h1[d], q1);
+          atomicAdd(&h2[d], q2);
+          atomicAdd(&hc[d], 1u);
+        }
       }
+      NS_STAMP(5 + 4 * lvl);
       ptx::cluster_sync();  // the cluster's histograms of this level are complete
-      if (tid < 256) {
+      NS_STAMP(6 + 4 * lvl);
+      {  // thread (b, h) gathers bucket b of the CTAs r = h, h + 2, ...: all loads in flight at once
+        const int b = tid & 255, h = tid >> 8;
+        uint32_t v0[8], v1[8], v2[8], nv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t r = (uint32_t)(h + 2 * j);
+          v0[j] = r < C ? ld_dsmem_u32(&h0[b], r) : 0u;
+          v1[j] = r < C ? ld_dsmem_u32(&h1[b], r) : 0u;
+          v2[j] = r < C ? ld_dsmem_u32(&h2[b], r) : 0u;
+          nv[j] = r < C ? ld_dsmem_u32(&hc[b], r) : 0u;
+        }
         u64 w = 0;
         uint32_t n_ = 0;
-        for (uint32_t r = 0; r < C; ++r) {
-          w += ld_dsmem_u64(&hw[tid], r);
-          n_ += ld_dsmem_u32(&hc[tid], r);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          w += (u64)v0[j] + ((u64)v1[j] << 14) + ((u64)v2[j] << 28);
+          n_ += nv[j];
         }
-        c->tw[tid] = w;
-        c->tc[tid] = n_;
+        if (h == 1) {
+          c->tw2[b] = w;
+          c->tc2[b] = n_;
+        }
+        __syncthreads();
+        if (h == 0) {
+          c->tw[b] = w + c->tw2[b];
+          c->tc[b] = n_ + c->tc2[b];
+        }
       }
       __syncthreads();
+      NS_STAMP(7 + 4 * lvl);
       if (warp == 0) {
         // lane l owns buckets 8l .. 8l+7; suffix sums over the lanes above it
         u64 sw = 0;
@@ -263,6 +345,7 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
         }
       }
       __syncthreads();
+      NS_STAMP(8 + 4 * lvl);
       prefix = (prefix << 8) | (u64)(uint32_t)c->sel_b;
       above = c->sel_above;
       cabove = c->sel_cabove;
@@ -283,6 +366,9 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
 
 }  // namespace
 }  // namespace pam
+
+static long long* g_nucset_dbg = nullptr;
+extern "C" void pam_dev_nucleus_set_clocks(long long* d_buf40) { g_nucset_dbg = d_buf40; }
 
 extern "C" int pam_nucleus_set_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int64_t n, double p,
                                          double* d_cutoff, int32_t* d_size, double* d_mass, int32_t* d_row_status,
@@ -305,6 +391,7 @@ extern "C" int pam_nucleus_set_batch_f64(const double* d_x, int64_t ld_x, int64_
   ka.size = d_size;
   ka.mass = d_mass;
   ka.status = d_row_status;
+  ka.dbg = g_nucset_dbg;
   const int smem = 2 * kLcap * 8 + (int)sizeof(NucSetCtl);
   const void* fn = (const void*)nucleus_set_kernel;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

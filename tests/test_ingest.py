@@ -90,12 +90,21 @@ def test_jsonl(tmp_path):
     assert e.value.vector_index == 0
 
 
+@pytest.mark.gpu
 def test_ingest_pinned(tmp_path):
+    """SPEC.md:543-551 ingest -> pinned host tensor -> one async H2D -> the batched kernel."""
     torch = pytest.importorskip("torch")
-    if not torch.cuda.is_available():
-        pytest.skip("pinned memory needs a CUDA device")
     x = np.arange(12, dtype=np.float32).reshape(3, 4)
     p = tmp_path / "p.lgt1"
     pam.write_lgt1(str(p), x)
     t = pam.ingest_pinned(str(p))
     assert t.is_pinned() and t.numpy().tobytes() == x.tobytes()
+    # the pinned upload feeds the fp32 batch entry point
+    rng = np.random.default_rng(3)
+    big = rng.normal(0, 3, (8, 4096)).astype(np.float32)
+    pam.write_lgt1(str(p), big)
+    tp = pam.ingest_pinned(str(p))
+    d = tp.to("cuda", non_blocking=True)
+    z, am, st = pam.cutmax_batch_device(d, pam.CutMaxParams())
+    torch.cuda.synchronize()
+    assert np.array_equal(am.cpu().numpy(), big.argmax(1)) and int(st.abs().sum()) == 0

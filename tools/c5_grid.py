@@ -17,6 +17,12 @@ import paper_2509_08383_b200 as pam
 from paper_2509_08383_b200 import workloads as W
 
 PEAK = 6547.5
+try:
+    import json
+    PEAK = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                            "MEASURED_PEAKS.json")))["hbm_gbs"])
+except Exception:
+    pass
 _flush = None
 
 
@@ -103,6 +109,13 @@ def main():
             gbs = B * (8 * 32768 + 9) / ms / 1e6
             print(f"| {'gumbel' if gumbel else 'beta-cut'} | {B} | 32768 | {ms * 1e3:.1f} | {B / ms * 1e3:.3g} | "
                   f"{gbs:.0f} | {'flush' if flush else 'stream'} |", flush=True)
+        ms = time_fn(lambda: pam.nucleus_set_batch_device(x, 0.9), 10, flush)
+        print(f"| nucleus set (cutoff/size/mass) | {B} | 32768 | {ms * 1e3:.1f} | {B / ms * 1e3:.3g} | "
+              f"{B * (8 * 32768 + 24) / ms / 1e6:.0f} | {'flush' if flush else 'stream'} |", flush=True)
+    x = torch.as_tensor(W.zipf_logits(1024, 151936, seed=3), device="cuda")
+    ms = time_fn(lambda: pam.nucleus_set_batch_device(x, 0.9), 5, False)
+    print(f"| nucleus set (cutoff/size/mass) | 1024 | 151936 | {ms * 1e3:.1f} | {1024 / ms * 1e3:.3g} | "
+          f"{1024 * (8 * 151936 + 24) / ms / 1e6:.0f} | stream |", flush=True)
 
 
 main()
