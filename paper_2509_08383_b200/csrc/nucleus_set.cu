@@ -18,7 +18,9 @@
 // the weights and counts of its slice's candidates (shared atomics; the two most
 // common digits of each warp step are pre-summed with REDUX), the cluster's histograms are summed through
 // distributed shared memory, and one warp scans the 256 buckets from the top for
-// the lowest non-empty bucket whose entries can still be inside.  Integer
+// the lowest non-empty bucket whose entries can still be inside; once at most 32
+// entries survive, they are gathered into one warp, which finishes exactly
+// (all-pairs mass above each, smallest inside key).  Integer
 // arithmetic throughout: every CTA takes the same decision, and the result is
 // bit-identical to the oracle's.
 //
@@ -70,6 +72,9 @@ struct NucSetCtl {
   uint32_t tc[256];
   u64 tw2[256];         // (second half of the gather)
   uint32_t tc2[256];
+  u64 cand_k[32];       // the last <= 32 candidates of this CTA's slice (key, mass) for the final gather
+  u64 cand_q[32];
+  uint32_t cand_n;
   u64 pmax;             // this CTA's max key / total weight / non-finite flag
   u64 pw;
   uint32_t pbad;
@@ -195,6 +200,7 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
     uint32_t cabove = 0;
     u64 eq_w = 0;
     uint32_t eq_c = 0;
+    int done_bits = 64;  // key bits fixed by the descent (64: all eight levels ran)
     for (int lvl = 0; lvl < 8; ++lvl) {
       const int shift = 56 - 8 * lvl;
       uint32_t* h0 = c->hp[lvl & 1][0];
@@ -223,17 +229,20 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
         // few distinct digits in the warp (the exponent levels, tie groups): one
         // REDUX pair and one atomic per digit; many: the buckets are spread and
         // direct atomics do not contend (a REDUX per distinct digit would serialise)
+        // (a group is worth its three REDUX only from 8 lanes up)
         const uint32_t d0 = __shfl_sync(0xffffffffu, d, __ffs(cm) - 1);
-        const uint32_t m0 = __ballot_sync(0xffffffffu, cand && d == d0);
+        uint32_t m0 = __ballot_sync(0xffffffffu, cand && d == d0);
         const uint32_t rest = cm & ~m0;
+        if (__popc(m0) < 8) m0 = 0u;
         uint32_t m1 = 0u, d1 = 0u;
-        if (rest) {
+        if (__popc(rest) >= 8) {  // warp-uniform
           d1 = __shfl_sync(0xffffffffu, d, __ffs(rest) - 1);
           m1 = __ballot_sync(0xffffffffu, cand && d == d1);
+          if (__popc(m1) < 8) m1 = 0u;
         }
         // q < 2^41 in three 14-bit pieces: a CTA's bucket sums stay below 2^32
         const uint32_t q0 = (uint32_t)q & 0x3fffu, q1 = (uint32_t)(q >> 14) & 0x3fffu, q2 = (uint32_t)(q >> 28);
-        {
+        if (m0) {  // warp-uniform
           const bool in0 = (m0 >> lane) & 1u;
           const uint32_t s0 = __reduce_add_sync(0xffffffffu, in0 ? q0 : 0u);
           const uint32_t s1 = __reduce_add_sync(0xffffffffu, in0 ? q1 : 0u);
@@ -353,8 +362,73 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
       eq_c = c->sel_c;
       // (the next level zeroes the other histogram buffer: a peer that still reads
       //  this level's has not reached the next cluster barrier)
+      if (lvl < 7 && eq_c <= 32u) {  // cluster-uniform: few survivors, finish without more levels
+        done_bits = 8 * (lvl + 1);
+        break;
+      }
     }
-    if (rank == 0 && tid == 0) {
+    if (done_bits < 64) {
+      // ---- final gather: the <= 32 entries whose key starts with `prefix` ----------
+      const int sh = 64 - done_bits;
+      if (tid == 0) c->cand_n = 0;
+      __syncthreads();
+      for (int i = tid; i < len; i += kNT) {
+        const u64 k = key[i], q = qw[i];
+        if (q > 0 && (k >> sh) == prefix) {
+          const uint32_t slot = atomicAdd(&c->cand_n, 1u);
+          if (slot < 32u) {
+            c->cand_k[slot] = k;
+            c->cand_q[slot] = q;
+          }
+        }
+      }
+      ptx::cluster_sync();
+      if (rank == 0 && warp == 0) {
+        // lane l takes the l-th candidate of the cluster (CTA order, then slot order)
+        const uint32_t cn = lane < (int)C ? ld_dsmem_u32(&c->cand_n, (uint32_t)lane) : 0u;
+        uint32_t inc = cn;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+          const uint32_t o = __shfl_up_sync(0xffffffffu, inc, m);
+          if (lane >= m) inc += o;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+        uint32_t rr = 0, jj = 0;
+        for (uint32_t r = 0; r < C; ++r) {
+          const uint32_t e = __shfl_sync(0xffffffffu, inc - cn, (int)r), n_ = __shfl_sync(0xffffffffu, cn, (int)r);
+          if ((uint32_t)lane >= e && (uint32_t)lane < e + n_) {
+            rr = r;
+            jj = (uint32_t)lane - e;
+          }
+        }
+        const bool have = (uint32_t)lane < total;
+        const u64 kl = have ? ld_dsmem_u64(&c->cand_k[jj], rr) : 0ull;
+        const u64 ql = have ? ld_dsmem_u64(&c->cand_q[jj], rr) : 0ull;
+        u64 al = above;  // mass strictly above this candidate
+        for (int m = 0; m < 32; ++m) {
+          const u64 km = __shfl_sync(0xffffffffu, kl, m), qm = __shfl_sync(0xffffffffu, ql, m);
+          if ((uint32_t)m < total && km > kl) al += qm;
+        }
+        const bool in = have && (double)al < pW;
+        u64 kc = in ? kl : ~0ull;  // the smallest inside key (the largest candidate is always inside)
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) {
+          const u64 o = __shfl_xor_sync(0xffffffffu, kc, m);
+          kc = o < kc ? o : kc;
+        }
+        const bool ge = have && kl >= kc;
+        u64 mq = ge ? ql : 0ull;
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) mq += __shfl_xor_sync(0xffffffffu, mq, m);
+        const uint32_t cnt = (uint32_t)__popc(__ballot_sync(0xffffffffu, ge));
+        if (lane == 0) {
+          if (a.cutoff) a.cutoff[row] = value_of(kc);
+          if (a.size) a.size[row] = (int32_t)(cabove + cnt);
+          if (a.mass) a.mass[row] = (double)(above + mq) / (double)W;
+          if (a.status) a.status[row] = PAM_OK;
+        }
+      }
+    } else if (rank == 0 && tid == 0) {
       if (a.cutoff) a.cutoff[row] = value_of(prefix);
       if (a.size) a.size[row] = (int32_t)(cabove + eq_c);
       if (a.mass) a.mass[row] = (double)(above + eq_w) / (double)W;
