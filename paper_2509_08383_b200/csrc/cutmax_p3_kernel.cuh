@@ -1,6 +1,7 @@
 // cutmax_p3_kernel.cuh — lean batched CutMax for a fixed odd power at every
 // iteration (p = 3, the headline schedule, and the Table-1 powers 5, 9, 13, 19;
-// PAPER.md:277-280), T >= 2, 16-byte aligned rows (TMA path).
+// PAPER.md:277-280) or, as P = 0, a per-iteration schedule p[t] (the HE
+// schedule of PAPER.md:291), T >= 2, 16-byte aligned rows (TMA path).
 //
 // Replaces core.cutmax for those parameters (Alg. 1
 // PAPER.md:51-72); every other case runs cutmax_rows_kernel (cutmax_kernel.cuh),
@@ -26,9 +27,31 @@
 
 namespace pam {
 
+// Runtime power -> compile-time constant for the even powers of the paper's HE
+// schedule (p = [16, 4, 4, 6]) and their neighbours, so that the
+// unrolled passes of the mixed-schedule kernel (P = 0) get a fully unrolled
+// square-and-multiply; any other power runs ipow's loop (same multiplications in
+// the same order either way).  p = 3 is left to the loop: the fixed-power kernel's
+// fused fma(z^2, z, -K') rounds once less than ipow(z, 3) - K'.
+template <int PP>
+struct PowC {
+  static constexpr int value = PP;
+};
+template <typename F>
+__device__ __forceinline__ void dispatch_power(const int p, F&& f) {
+  switch (p) {
+    case 2: f(PowC<2>()); break;
+    case 4: f(PowC<4>()); break;
+    case 6: f(PowC<6>()); break;
+    case 8: f(PowC<8>()); break;
+    case 16: f(PowC<16>()); break;
+    default: f(PowC<0>()); break;
+  }
+}
+
 // P: the odd power at every iteration (3: analytic normaliser; other P: an
 // explicit sum of Y^(T+1) -- one more pass and exchange -- before the fused
-// last pass).
+// last pass).  P = 0: a per-iteration schedule p[t] (any powers; explicit sum).
 template <typename Elem, int NTG, int E, int MINB = 0, int P = 3>
 __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, NTG, E>()))
     cutmax_lean_kernel(const CutmaxArgs a) {
@@ -379,12 +402,14 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
       PAM_TRACE(tr, 13 + t);
       const bool need3 = (P == 3) && (t + 2 == T);
       Elem sa = 0, sb = 0, qa = 0, qb = 0, ra = 0, rb = 0;
-      auto pass = [&](auto r3_c) {
+      const int pt = P > 0 ? P : a.rp.p[t];
+      auto pass = [&](auto r3_c, auto pc) {
         constexpr bool R3 = decltype(r3_c)::value;
+        constexpr int PP = P > 0 ? P : decltype(pc)::value;
 #pragma unroll
         for (int i = 0; i < E; i += 2) {
-          const Elem d0 = cutmax_update<Elem, P>(v[i], ke, be, kn, P);
-          const Elem d1 = cutmax_update<Elem, P>(v[i + 1], ke, be, kn, P);
+          const Elem d0 = cutmax_update<Elem, PP>(v[i], ke, be, kn, pt);
+          const Elem d1 = cutmax_update<Elem, PP>(v[i + 1], ke, be, kn, pt);
           v[i] = d0;
           v[i + 1] = d1;
           if (R3) {
@@ -411,10 +436,12 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
           }
         }
       };
-      if (need3)
-        pass(BoolC<true>());
+      if (P == 0)
+        dispatch_power(pt, [&](auto pc) { pass(BoolC<false>(), pc); });
+      else if (need3)
+        pass(BoolC<true>(), PowC<P>());
       else
-        pass(BoolC<false>());
+        pass(BoolC<false>(), PowC<P>());
       PAM_TRACE(tr, 5 + 2 * t);
       auto side = [&]() {
         if (t == 0) issue_upto(nch / 2);
@@ -441,7 +468,7 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         long long ci = 0;
         const double2 r = need3 ? xch_wait<kSum3>(r3, ci, cb, xround, C, gtid)
                                 : xch_wait<kSum2>(r3, ci, cb, xround, C, gtid);
-        const double wd = (double)cutmax_update<Elem, P>((Elem)cb->p3_w, ke, be, kn, P);
+        const double wd = (double)cutmax_update<Elem, P>((Elem)cb->p3_w, ke, be, kn, pt);
         const double m = mph();
         __syncwarp();
         if (gtid == 0) {
@@ -461,18 +488,26 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
     Elem ke, be, re;
     control(T - 1, ke, be, re);
     const Elem kz = (Elem)0;  // kshift[T] = 0
+    const int pl = P > 0 ? P : a.rp.p[T - 1];
     if (!(re == re)) {  // explicit sum of Y: P != 3, or the analytic total is not finite (rare); cluster-uniform
       Elem ta = 0, tb = 0;
+      auto sumy = [&](auto pc) {
+        constexpr int PP = P > 0 ? P : decltype(pc)::value;
 #pragma unroll
-      for (int i = 0; i < E; i += 2) {
-        const Elem y0 = cutmax_update<Elem, P>(v[i], ke, be, kz, P);
-        const Elem y1 = cutmax_update<Elem, P>(v[i + 1], ke, be, kz, P);
-        if (real(i)) ta += y0;
-        if (real(i + 1)) tb += y1;
-      }
+        for (int i = 0; i < E; i += 2) {
+          const Elem y0 = cutmax_update<Elem, PP>(v[i], ke, be, kz, pl);
+          const Elem y1 = cutmax_update<Elem, PP>(v[i + 1], ke, be, kz, pl);
+          if (real(i)) ta += y0;
+          if (real(i + 1)) tb += y1;
+        }
+      };
+      if (P == 0)
+        dispatch_power(pl, sumy);
+      else
+        sumy(PowC<P>());
       const double tot = cluster_sum2<NTG>((double)ta + (double)tb, 0.0, cb, xround, rank, C, gtid).x;
       if (warp == 0) {
-        const double total = tot - mph() * (double)cutmax_update<Elem, P>((Elem)cb->p3_w, ke, be, kz, P);
+        const double total = tot - mph() * (double)cutmax_update<Elem, P>((Elem)cb->p3_w, ke, be, kz, pl);
         int st = cb->p3_st;
         const double rn = finish_total(total, st);
         __syncwarp();
@@ -500,15 +535,16 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
     Elem bestv = -INFINITY;
     int besto = 0;  // register slot of the best element (compile-time immediates)
     Elem sa = 0, qa = 0;
-    auto last_pass = [&](auto merged_c) {
+    auto last_pass = [&](auto merged_c, auto pc) {
       constexpr bool MERGED = decltype(merged_c)::value;  // X(next) swapped in (compile-time: no per-slot branch)
+      constexpr int PP = P > 0 ? P : decltype(pc)::value;
 #pragma unroll
       for (int kk = 0; kk < NV; ++kk) {
         const int li0 = (kk * NTG + gtid) * VEC;
         Elem o[VEC];
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          const Elem y = cutmax_update<Elem, P>(v[kk * VEC + j], ke, be, kz, P);
+          const Elem y = cutmax_update<Elem, PP>(v[kk * VEC + j], ke, be, kz, pl);
           if (y > bestv) {  // slots in increasing element order: strict > keeps the lowest index
             bestv = y;
             besto = kk * VEC + j;
@@ -540,10 +576,16 @@ __global__ void __launch_bounds__(NTG, (MINB > 0 ? MINB : min_blocks_for<Elem, N
         }
       }
     };
-    if (has_next)
-      last_pass(BoolC<true>());
-    else
-      last_pass(BoolC<false>());
+    if (P == 0) {
+      if (has_next)
+        dispatch_power(pl, [&](auto pc) { last_pass(BoolC<true>(), pc); });
+      else
+        last_pass(BoolC<false>(), PowC<0>());
+    } else if (has_next) {
+      last_pass(BoolC<true>(), PowC<P>());
+    } else {
+      last_pass(BoolC<false>(), PowC<P>());
+    }
     ptx::fence_proxy_async_smem();  // Z writes -> visible to the TMA engine after the barrier
     PAM_TRACE(tr, 24);
     double best = (double)bestv;

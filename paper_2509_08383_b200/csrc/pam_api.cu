@@ -277,16 +277,25 @@ int uniform_p(const pam_cutmax_params* prm) {
 // power p at every iteration (nullptr: none compiled).  Used for T >= 2,
 // aligned rows, no early stopping, unless switched off (pam_set_lean_p3(0)).
 const LeanVariant* find_lean(int elem_bytes, const Variant& v, int p) {
-  if (!g_ovr.lean.load() || p <= 0) return nullptr;
-  const LeanVariant* tabs[2] = {elem_bytes == 8 ? kCutmaxP3F64 : kCutmaxP3F32,
-                                elem_bytes == 8 ? kCutmaxPGenF64 : nullptr};
-  const int cnts[2] = {elem_bytes == 8 ? kNumCutmaxP3F64 : kNumCutmaxP3F32, elem_bytes == 8 ? kNumCutmaxPGenF64 : 0};
-  for (int k = 0; k < 2; ++k)
+  if (!g_ovr.lean.load() || p < 0) return nullptr;  // p = 0: a mixed schedule (the P = 0 kernels)
+  const LeanVariant* tabs[3] = {elem_bytes == 8 ? kCutmaxP3F64 : kCutmaxP3F32,
+                                elem_bytes == 8 ? kCutmaxPGenF64 : nullptr, elem_bytes == 8 ? kCutmaxPMixF64 : nullptr};
+  const int cnts[3] = {elem_bytes == 8 ? kNumCutmaxP3F64 : kNumCutmaxP3F32, elem_bytes == 8 ? kNumCutmaxPGenF64 : 0,
+                       elem_bytes == 8 ? kNumCutmaxPMixF64 : 0};
+  for (int k = 0; k < 3; ++k)
     for (int i = 0; i < cnts[k]; ++i) {
       const LeanVariant& l = tabs[k][i];
       if (l.p == p && l.ntg == v.ntg && l.e == v.e && l.minb == v.minb) return &l;
     }
   return nullptr;
+}
+
+// The fixed-power kernel of the schedule if one is compiled, else the
+// mixed-schedule kernel (P = 0: any powers, e.g. the HE schedule p = [16, 4, 4, 6]).
+const LeanVariant* find_lean_any(int elem_bytes, const Variant& v, const pam_cutmax_params* prm) {
+  const int up = uniform_p(prm);
+  const LeanVariant* lv = up > 0 ? find_lean(elem_bytes, v, up) : nullptr;
+  return lv ? lv : find_lean(elem_bytes, v, 0);
 }
 
 // ---- warp-per-row kernels ------------------------------------------------------
@@ -371,7 +380,7 @@ int cutmax_batch_impl(const Elem* d_x, int64_t ld_x, int64_t B, int64_t n, const
   const void* fn = g.var->fn[flavour];
   // p = 3 everywhere, T >= 2, aligned rows: the lean kernel of the same geometry
   if (flavour != 2 && tma && prm->T >= 2)
-    if (const LeanVariant* lv = find_lean((int)sizeof(Elem), *g.var, uniform_p(prm))) fn = lv->fn;
+    if (const LeanVariant* lv = find_lean_any((int)sizeof(Elem), *g.var, prm)) fn = lv->fn;
   // the row buffer is sized for the full capacity even without TMA so the
   // occupancy (and the chooser's estimate) does not depend on alignment
   const int smem = smem_bytes(*g.var);
@@ -787,7 +796,7 @@ int pam_query_launch(int dtype_bytes, int64_t B, int64_t n, const pam_cutmax_par
   info->groups = 1;
   const VariantTable& tab = kCutmaxTables[dtype_bytes == 8 ? 1 : 0];
   info->kernel_id = (int)(g.var - tab.v) + 100 * flavour;
-  if (flavour != 2 && prm && prm->T >= 2 && find_lean(dtype_bytes, *g.var, uniform_p(prm)))
+  if (flavour != 2 && prm && prm->T >= 2 && find_lean_any(dtype_bytes, *g.var, prm))
     info->kernel_id += 1000;  // lean kernel (aligned rows)
   return PAM_OK;
 }

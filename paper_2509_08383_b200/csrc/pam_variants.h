@@ -53,6 +53,8 @@ extern const LeanVariant kCutmaxP3F32[];
 extern const int kNumCutmaxP3F32;
 extern const LeanVariant kCutmaxPGenF64[];
 extern const int kNumCutmaxPGenF64;
+extern const LeanVariant kCutmaxPMixF64[];  // P = 0: per-iteration schedule p[t]
+extern const int kNumCutmaxPMixF64;
 
 extern const Variant kCutmaxVariantsF64[];
 extern const int kNumCutmaxVariantsF64;

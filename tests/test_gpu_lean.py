@@ -153,3 +153,43 @@ def test_lean_table1_powers_vs_oracle(cuda, pam, orc, n, T, p, c):
     tol = 1e-12 * max(1.0, p ** T / 81)
     worst = max(float(np.max(np.abs(zz[r] - zr[r])) / np.max(np.abs(zr[r]))) for r in np.nonzero(ok)[0])
     assert worst <= tol, worst
+
+
+@pytest.mark.parametrize("n", [151936, 32768])
+@pytest.mark.parametrize("sched", [
+    dict(p=[16, 4, 4, 6], c=[5.0, 3.0, 3.0, 3.0], T=4, checked=False),  # the HE schedule
+    dict(p=[3, 5, 3], c=[5.0, 8.0, 5.0], T=3),                          # mixed odd powers (ipow loop)
+    dict(p=4, c=6.0, T=3, checked=False),                                 # one even power everywhere
+    dict(p=7, c=10.0, T=3),                                               # an odd power with no fixed-P kernel
+    dict(p=[8, 2], c=[6.0, 4.0], T=2, checked=False),
+])
+def test_lean_mixed_schedule_vs_oracle(cuda, pam, orc, n, sched):
+    """The mixed-schedule lean kernel (P = 0: per-iteration powers, unrolled
+    square-and-multiply for the even powers of the HE schedule, ipow's loop for
+    the rest) against the oracle and against the general kernel."""
+    torch = cuda
+    B = 100
+    x = W.gaussian(B, n, seed=n % 97 + len(str(sched)))
+    prm = pam.CutMaxParams(**sched)
+    xt = torch.as_tensor(x, device="cuda")
+    z, am, st = pam.cutmax_batch_device(xt, prm)
+    torch.cuda.synchronize()
+    assert 1000 <= pam.launch_info(8, B, n, prm)["kernel_id"] < 2000, "lean kernel not selected"
+    with pam.general_p3_kernel():
+        zg, amg, stg = pam.cutmax_batch_device(xt, prm)
+        assert pam.launch_info(8, B, n, prm)["kernel_id"] < 1000
+    torch.cuda.synchronize()
+    zr, amr, sr = orc.cutmax_batch(x[:24], prm.lower())
+    st_, am_ = st.cpu().numpy(), am.cpu().numpy()
+    assert np.array_equal(st_[:24], sr) and np.array_equal(st_, stg.cpu().numpy())
+    ok = (st_ & 0xFF) == 0
+    assert bool(ok.any())
+    assert np.array_equal(am_[:24][ok[:24]], amr[ok[:24]]) and np.array_equal(am_[ok], amg.cpu().numpy()[ok])
+    ps = sched["p"] if isinstance(sched["p"], list) else [sched["p"]] * sched["T"]
+    tol = 1e-12 * max(1.0, float(np.prod(ps)) / 81.0)
+    zz = z.cpu().numpy()
+    worst = max(float(np.max(np.abs(zz[r] - zr[r])) / np.max(np.abs(zr[r]))) for r in np.nonzero(ok[:24])[0])
+    assert worst <= tol, worst
+    zg_ = zg.cpu().numpy()
+    worst_g = max(float(np.max(np.abs(zz[r] - zg_[r])) / np.max(np.abs(zg_[r]))) for r in np.nonzero(ok)[0])
+    assert worst_g <= tol, worst_g
