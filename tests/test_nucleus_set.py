@@ -145,3 +145,25 @@ def test_gpu_errors_and_strided(cuda, pam):
     assert np.array_equal(size.cpu().numpy(), rs) and np.array_equal(cut.cpu().numpy(), rc)
     d = pam.nucleusSet(view[0].cpu().numpy(), 0.8)
     assert d["size"] == rs[0] and d["cutoff"] == rc[0]
+
+
+@pytest.mark.gpu
+def test_gpu_fuzz(cuda, pam):
+    """Seeded random shapes, scales, tie densities and p: every cluster size, n
+    down to 1, rows with a handful of distinct values."""
+    rng = np.random.default_rng(20250918)
+    for case in range(40):
+        n = int(rng.choice([1, 2, 7, 100, 1000, 4097, 12288, 12289, 30000, 60000, 100003]))
+        B = int(rng.integers(1, 9))
+        kind = case % 4
+        if kind == 0:
+            x = rng.normal(0.0, float(rng.choice([1e-3, 1.0, 3.0, 30.0])), (B, n))
+        elif kind == 1:
+            x = np.round(rng.normal(0.0, 2.0, (B, n)), int(rng.integers(0, 3)))  # heavy ties
+        elif kind == 2:
+            x = -1.1 * np.log(rng.permuted(np.tile(np.arange(1, n + 1, dtype=np.float64), (B, 1)), axis=1)) \
+                + rng.normal(0, 0.5, (B, n))
+        else:
+            x = rng.normal(0.0, 3.0, (B, n)) + float(rng.choice([-1e6, 0.0, 1e3]))
+        p = float(rng.choice([0.01, 0.3, 0.5, 0.9, 0.95, 0.999]))
+        _gpu_vs_oracle(cuda, pam, np.ascontiguousarray(x), p)

@@ -40,12 +40,11 @@ def main():
         x, kind = rows(rng, B, n)
         prm = pam.CutMaxParams(p=3, c=c, T=T)
         zr, amr, sr = orc.cutmax_batch(x, prm.lower())
-        for k in ("rows", "ahead"):
-            if k == "ahead":
-                os.environ["PAM_ENABLE_AHEAD"] = "1"
-            z, am, st = pam.cutmax_batch_device(torch.as_tensor(x, device="cuda"), prm)
-            torch.cuda.synchronize()
-            os.environ.pop("PAM_ENABLE_AHEAD", None)
+        for k in ("product", "general"):  # the product path (lean / warp kernel where they apply) and the general kernel
+            import contextlib
+            with (pam.general_p3_kernel() if k == "general" else contextlib.nullcontext()):
+                z, am, st = pam.cutmax_batch_device(torch.as_tensor(x, device="cuda"), prm)
+                torch.cuda.synchronize()
             z, am, st = z.cpu().numpy(), am.cpu().numpy(), st.cpu().numpy()
             ok = sr == 0
             err = max([float(np.max(np.abs(z[r] - zr[r])) / np.max(np.abs(zr[r]))) for r in np.nonzero(ok)[0]], default=0.0)
