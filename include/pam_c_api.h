@@ -185,7 +185,7 @@ int pam_gumbel_sample_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int6
  * their softmax mass; x_k is inside <=> x_k >= cutoff[r].  The cumulative-mass
  * step is a cluster-wide histogram scan (radix select) over 40-bit fixed-point
  * masses floor(exp(x - max) 2^40 + 1/2), which makes the result independent of
- * the summation order (bit-exact against the oracle).  n <= 196608.  Outputs
+ * the summation order (bit-exact against the oracle).  n <= 180224.  Outputs
  * are nullable.  Replaces the nucleus ground truth of sampling.violationExperiment
  * (SPEC.md:447-455, 464).  Row status: PAM_OK or PAM_ERR_NON_FINITE. */
 int pam_nucleus_set_batch_f64(const double* d_x, int64_t ld_x, int64_t B, int64_t n, double p,

@@ -13,8 +13,9 @@
 //   v is inside the nucleus  <=>  (double)A(v) < p * (double)W   (ties share A);
 //   cutoff = the smallest inside value, size = #{x_i >= cutoff, w_i > 0},
 //   mass = (A(cutoff) + weight of the entries equal to cutoff) / W.
-// inside() is monotone in v, so the cutoff is found by descending the bits of
-// an order-preserving 64-bit key of x, 8 bits per level: each CTA histograms
+// inside() is monotone in v, so the cutoff is found by descending first (small
+// clusters) 1024 linear buckets of max - x, then the bits of an
+// order-preserving 64-bit key of x, 8 bits per level: each CTA histograms
 // the weights and counts of its slice's candidates (shared atomics; the two most
 // common digits of each warp step are pre-summed with REDUX), the cluster's histograms are summed through
 // distributed shared memory, and one warp scans the 256 buckets from the top for
@@ -24,8 +25,8 @@
 // arithmetic throughout: every CTA takes the same decision, and the result is
 // bit-identical to the oracle's.
 //
-// One row per cluster (C = 1..16 CTAs, slice keys and weights resident in
-// shared memory: 16 bytes per element), rows strided over the persistent
+// One row per cluster (C = 1..16 CTAs of <= 11264 entries, slice keys and weights
+// resident in shared memory: 16 bytes per element), rows strided over the persistent
 // clusters.  HBM traffic: 8n bytes read per row, 24 bytes written.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -43,7 +44,7 @@ namespace {
 
 typedef unsigned long long u64;
 constexpr int kNT = 512;
-constexpr int kLcap = 12288;  // elements per CTA: 2 x 96 KB of shared memory
+constexpr int kLcap = 11264;  // elements per CTA: 2 x 88 KB of shared memory
 constexpr int kWBits = 40;
 
 struct NucSetArgs {
@@ -72,6 +73,12 @@ struct NucSetCtl {
   uint32_t tc[256];
   u64 tw2[256];         // (second half of the gather)
   uint32_t tc2[256];
+  // level A: histogram over 1024 linear buckets of max - x (1/16 wide): three
+  // 14-bit mass pieces and a count per bucket
+  uint32_t ha[4][1024];
+  u64 scan_w[16];       // level A block scan: per-warp totals
+  uint32_t scan_c[16];
+  int scan_b[16];
   u64 cand_k[32];       // the last <= 32 candidates of this CTA's slice (key, mass) for the final gather
   u64 cand_q[32];
   uint32_t cand_n;
@@ -116,6 +123,9 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
   const int64_t base = (int64_t)rank * a.L;
   const int64_t rem = a.n - base;
   const int len = rem <= 0 ? 0 : (rem < a.L ? (int)rem : a.L);
+  // level A pays for its 1024-bucket gather only in small clusters (16 peers: 128
+  // DSMEM loads per thread); larger ones run the key descent from the top byte
+  const bool useA = C <= 4;
 
   for (int64_t row = cid; row < a.B; row += ncl) {
     if (tid == 0) {
@@ -123,6 +133,8 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
       c->pw = 0;
       c->pbad = 0;
     }
+    if (useA)
+      for (int b = tid; b < 4 * 1024; b += kNT) (&c->ha[0][0])[b] = 0u;
     __syncthreads();
     NS_STAMP(0);
     // ---- keys, row maximum, non-finite check ---------------------------------
@@ -182,6 +194,13 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
         const u64 q = t < -64.0 ? 0ull : (u64)(e * 0x1p40 + 0.5);
         qw[i] = q;
         ws += q;
+        if (useA && q > 0) {  // level A histogram (q > 0 => t > -29: bucket < 1024)
+          const int bA = (int)(-t * 16.0);
+          atomicAdd(&c->ha[0][bA], (uint32_t)q & 0x3fffu);
+          atomicAdd(&c->ha[1][bA], (uint32_t)(q >> 14) & 0x3fffu);
+          atomicAdd(&c->ha[2][bA], (uint32_t)(q >> 28));
+          atomicAdd(&c->ha[3][bA], 1u);
+        }
       }
 #pragma unroll
       for (int m = 16; m > 0; m >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, m);
@@ -195,13 +214,100 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
     for (int m = 16; m > 0; m >>= 1) W += __shfl_xor_sync(0xffffffffu, W, m);
     const double pW = a.p * (double)W;
 
-    // ---- radix descent: 8 levels of 8 key bits ---------------------------------
+    // ---- level A: 1024 linear buckets of max - x (value space) -------------------
+    // The top bytes of the key are sign and exponent: nearly every entry shares
+    // them, so two radix levels would pass over the whole slice for nothing.  A
+    // monotone value-space split spreads the entries instead; the key descent
+    // then starts below the bytes the chosen bucket's bounds have in common.
     u64 prefix = 0, above = 0;  // above = A(everything in the current bucket's range)
     uint32_t cabove = 0;
     u64 eq_w = 0;
     uint32_t eq_c = 0;
-    int done_bits = 64;  // key bits fixed by the descent (64: all eight levels ran)
-    for (int lvl = 0; lvl < 8; ++lvl) {
+    int selA = 0;
+    if (useA) {
+      // thread t gathers buckets 2t and 2t + 1 (ascending bucket = descending x)
+      u64 w2[2] = {0, 0};
+      uint32_t c2[2] = {0, 0};
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int b = 2 * tid + j;
+        for (uint32_t r0 = 0; r0 < C; r0 += 4) {
+          uint32_t v[4][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[u][q] = r0 + u < C ? ld_dsmem_u32(&c->ha[q][b], r0 + u) : 0u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            w2[j] += (u64)v[u][0] + ((u64)v[u][1] << 14) + ((u64)v[u][2] << 28);
+            c2[j] += v[u][3];
+          }
+        }
+      }
+      // block exclusive scan of (mass, count) over the 1024 buckets
+      u64 iw = w2[0] + w2[1];
+      uint32_t ic = c2[0] + c2[1];
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const u64 ow = __shfl_up_sync(0xffffffffu, iw, m);
+        const uint32_t oc = __shfl_up_sync(0xffffffffu, ic, m);
+        if (lane >= m) {
+          iw += ow;
+          ic += oc;
+        }
+      }
+      if (lane == 31) {
+        c->scan_w[warp] = iw;
+        c->scan_c[warp] = ic;
+      }
+      __syncthreads();
+      u64 xw = iw - (w2[0] + w2[1]);  // exclusive within the warp
+      uint32_t xc = ic - (c2[0] + c2[1]);
+      for (int w = 0; w < warp; ++w) {
+        xw += c->scan_w[w];
+        xc += c->scan_c[w];
+      }
+      // the largest bucket index that is non-empty and whose top entry is inside
+      int mine = -1;
+      if (c2[0] > 0 && (double)xw < pW) mine = 2 * tid;
+      if (c2[1] > 0 && (double)(xw + w2[0]) < pW) mine = 2 * tid + 1;
+      const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)(mine + 1)) - 1;
+      if (lane == 0) c->scan_b[warp] = wmax;
+      __syncthreads();
+      int sel = -1;
+      for (int w = 0; w < kNT / 32; ++w) sel = c->scan_b[w] > sel ? c->scan_b[w] : sel;
+      if (mine == sel && sel >= 0) {
+        const int j = sel & 1;
+        c->sel_b = sel;
+        c->sel_above = xw + (j ? w2[0] : 0ull);
+        c->sel_cabove = xc + (j ? c2[0] : 0u);
+        c->sel_w = w2[j];
+        c->sel_c = c2[j];
+      }
+      __syncthreads();
+      selA = c->sel_b;
+      above = c->sel_above;
+      cabove = c->sel_cabove;
+      eq_w = c->sel_w;
+      eq_c = c->sel_c;
+    }
+    auto in_selA = [&](const u64 k) { return !useA || (int)((mx - value_of(k)) * 16.0) == selA; };
+    // ---- key descent inside that bucket: 8 key bits per level ---------------------
+    int done_bits = 64;  // key bits fixed by the descent (64: all levels ran; 0: level A alone)
+    int lvl0 = 0;
+    if (!useA) {
+      // (the descent starts at the top byte with every entry of positive mass a candidate)
+    } else if (eq_c <= 32u) {
+      done_bits = 0;
+      lvl0 = 8;
+    } else {  // the bucket's entries lie in [lo, hi] (bounds widened past any rounding of max - x)
+      const double delta = (fabs(mx) + 64.0) * 0x1p-48;
+      const u64 klo = key_of(mx - (double)(selA + 1) * 0.0625 - delta), khi = key_of(mx - (double)selA * 0.0625 + delta);
+      const int shared = (klo == khi) ? 64 : __clzll((long long)(klo ^ khi));
+      lvl0 = shared / 8 > 7 ? 7 : shared / 8;
+      prefix = lvl0 ? khi >> (64 - 8 * lvl0) : 0ull;
+    }
+    for (int lvl = lvl0; lvl < 8; ++lvl) {
       const int shift = 56 - 8 * lvl;
       uint32_t* h0 = c->hp[lvl & 1][0];
       uint32_t* h1 = c->hp[lvl & 1][1];
@@ -222,7 +328,7 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
           k = key[i];
           q = qw[i];
         }
-        const bool cand = q > 0 && (lvl == 0 || (k >> (shift + 8)) == prefix);
+        const bool cand = q > 0 && (lvl == 0 || (k >> (shift + 8)) == prefix) && in_selA(k);
         const uint32_t cm = __ballot_sync(0xffffffffu, cand);
         if (cm == 0u) continue;  // warp-uniform
         const uint32_t d = (uint32_t)(k >> shift) & 255u;
@@ -374,7 +480,7 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
       __syncthreads();
       for (int i = tid; i < len; i += kNT) {
         const u64 k = key[i], q = qw[i];
-        if (q > 0 && (k >> sh) == prefix) {
+        if (q > 0 && (done_bits == 0 || (k >> sh) == prefix) && in_selA(k)) {
           const uint32_t slot = atomicAdd(&c->cand_n, 1u);
           if (slot < 32u) {
             c->cand_k[slot] = k;
@@ -451,7 +557,7 @@ extern "C" int pam_nucleus_set_batch_f64(const double* d_x, int64_t ld_x, int64_
   if (B < 0 || n < 1 || ld_x < n || (B > 0 && !d_x)) return PAM_ERR_BAD_ARGUMENT;
   if (!(p > 0.0 && p < 1.0)) return PAM_ERR_DOMAIN;
   if (B == 0) return PAM_OK;
-  if (n > (int64_t)16 * kLcap) return PAM_ERR_UNSUPPORTED;  // 196608 entries per row
+  if (n > (int64_t)16 * kLcap) return PAM_ERR_UNSUPPORTED;  // 180224 entries per row
   int C = 1;
   while ((int64_t)C * kLcap < n) C *= 2;
   NucSetArgs ka;
