@@ -123,9 +123,9 @@ __global__ void __launch_bounds__(kNT, 1) nucleus_set_kernel(const NucSetArgs a)
   const int64_t base = (int64_t)rank * a.L;
   const int64_t rem = a.n - base;
   const int len = rem <= 0 ? 0 : (rem < a.L ? (int)rem : a.L);
-  // level A pays for its 1024-bucket gather only in small clusters (16 peers: 128
+  // level A pays for its 1024-bucket gather only in clusters of up to 8 CTAs (16 peers: 128
   // DSMEM loads per thread); larger ones run the key descent from the top byte
-  const bool useA = C <= 4;
+  const bool useA = C <= 8;
 
   for (int64_t row = cid; row < a.B; row += ncl) {
     if (tid == 0) {
